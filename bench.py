@@ -1,0 +1,416 @@
+"""Benchmark of the neural-preconditioned coupled FGMRES solve on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg2]
+
+A step is one full coupled solve (outer FGMRES(restart) with the ILU(0) 1D
+block and the 3-step inner FGMRES on C preconditioned by the Jacobi(2,2/3)-
+wrapped TF32 U-Net) of the workload's systems, inputs resident in HBM.
+N > 1 (torchrun): every rank solves its own replica of the workload (the
+path has no exchange step: replicas only); value is
+the total solves/s over all ranks, timed on the device, max over ranks.
+
+Extras on the one JSON line: roofline of the dominant kernel (the tcgen05
+conv layer with the largest share), the coupled-SpMV HBM roofline, the
+end-to-end drop-in API number (host buffers, copies inside the timed
+region), the CPU oracle baseline, clocks sampled during the timed region,
+and the number of our kernels launched.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "preconditioned FGMRES solves/sec + applies/sec at 1 B200; % HBM/tensor roofline"
+# outer iterations of the full solve, from the parity-checked GPU run (the
+# reference arm times a bounded sample of iterations and extrapolates)
+EXPECTED_ITERS = {"cfg1": None, "cfg2": None, "cfg3": None, "cfg4": None}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def flush_l2(buf):
+    buf.add_(1.0)  # 256 MiB write > 126 MB L2
+
+
+def measure_tf32_peak():
+    """cuBLAS TF32 GEMM 8192^3, best of 5 (the tensor-core denominator for kind::tf32)."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = True
+    a = torch.randn(8192, 8192, device="cuda")
+    b = torch.randn(8192, 8192, device="cuda")
+    for _ in range(2):
+        a @ b
+    best = 0.0
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        a @ b
+        e.record()
+        e.synchronize()
+        best = max(best, 2 * 8192 ** 3 / (s.elapsed_time(e) * 1e-3) / 1e12)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    del a, b
+    return best
+
+
+def conv_layer_times(n, reps=20):
+    """Average device time of each tcgen05 conv layer of the forward at size n."""
+    import numpy as np
+    import torch
+    from paper_2505_08491_b200 import _ext, neural
+    lib = _ext.lib()
+    m, q = n // 2, n // 4
+    layers = [("enc1b", n, 16, 32, 0), ("enc2", n, 32, 64, 1), ("enc3", m, 64, 128, 1),
+              ("bottleneck", q, 128, 128, 0), ("dec2", m, 128, 64, 0), ("dec1", n, 64, 32, 0)]
+    out = {}
+    rng = np.random.default_rng(0)
+    for name, S, cin, cout, pool in layers:
+        X = torch.as_tensor(rng.standard_normal(cin * S ** 3).astype(np.float32), device="cuda")
+        W = torch.as_tensor(neural.pack_conv(rng.standard_normal((cout, cin, 3, 3, 3)) * 0.05, 0).ravel(),
+                            device="cuda")
+        So = S // 2 if pool else S
+        Y = torch.empty(cout * So ** 3, dtype=torch.float32, device="cuda")
+        st = _ext.stream()
+
+        def run():
+            _ext.check(lib.mdp_conv3_layer(0, 1, S, cin, cout, X.data_ptr(), cin // 4, 0, W.data_ptr(), None, 1,
+                                           Y.data_ptr(), cout // 4, 0, pool, st))
+        run()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            run()
+        e.record()
+        e.synchronize()
+        ms = s.elapsed_time(e) / reps
+        flops = 2.0 * S ** 3 * cin * cout * 27
+        out[name] = {"ms": ms, "flops": flops, "tflops": flops / (ms * 1e-3) / 1e12, "S": S}
+    return out
+
+
+def spmv_roofline(solver, reps=50):
+    """Coupled SpMV: algorithmic bytes 16 (N3 + N1) + 40 Q per system."""
+    import torch
+    p = solver.prob
+    X = p.zeros().normal_()
+    Y = p.zeros()
+    for _ in range(3):
+        solver.A.matvec(X, Y)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        solver.A.matvec(X, Y)
+    e.record()
+    e.synchronize()
+    ms = s.elapsed_time(e) / reps
+    nbytes = sum(16 * (p.n3 + int(n1)) for n1 in p.n1) + 40 * p.Qtot
+    return ms, nbytes
+
+
+def run_reference(args):
+    """CPU arm: the oracle restatement of the reference path on the host cores."""
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2505_08491_b200 import configs
+    wl = configs.CONFIGS[args.workload]()
+    osys = oracle_system(args.workload)
+    spec = {"type": "neural", "params": oracle.noisy_params(wl.cnn_seed), "smoothing": wl.smoothing}
+    sample = args.ref_iters
+    times = []
+    for step in range(args.warmup + args.steps):
+        st = oracle.CoupledStrategy(tol=wl.tol, maxit=sample, restart=wl.restart,
+                                    inner_iterations=wl.inner_iterations, three_d=spec)
+        t0 = time.perf_counter()
+        oracle.solve_coupled(osys, st)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    per_iter = statistics.median(times) / sample
+    full = EXPECTED_ITERS.get(args.workload) or wl.maxit
+    value = 1.0 / (per_iter * full) * len(wl.systems)
+    cores = len(os.sched_getaffinity(0))
+    line = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": statistics.median(times) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE graphs)",
+            "config": {"workload": args.workload, **wl.meta}, "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port",
+                             "sample": f"{sample} outer iterations of the oracle coupled solve per step, "
+                                       f"extrapolated to {full} iterations (x{len(wl.systems)} systems)"},
+            "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def oracle_system(name):
+    """The workload's first system built by the oracle from the same seeded graph."""
+    from oracle import problem as OP
+    if name == "cfg1":
+        g = OP.segment_graph([0.5, 0.5, 0.1], [0.5, 0.5, 0.9], 0.02)
+        return OP.assemble_coupled_system(OP.StructuredGrid(17), g, OP.PhysicalParams(epsilon=0.02, beta=1.0),
+                                          n_circle=8, elems_per_edge=32, bc3d="dirichlet", f1d=1.0)
+    if name == "cfg2":
+        g = OP.random_tree(8, 1, 0.015)
+        return OP.assemble_coupled_system(OP.StructuredGrid(33), g, OP.PhysicalParams(epsilon=0.015, beta=1.0),
+                                          n_circle=8, elems_per_edge=16, bc3d="dirichlet", f1d=1.0)
+    raise ValueError(f"no oracle builder for {name}")
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2505_08491_b200 import _ext, configs, harness, neural
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _ext.lib()
+    wl = configs.CONFIGS[args.workload]()
+    if args.maxit:
+        wl.maxit = args.maxit
+    params = neural.perturbed_params(wl.cnn_seed)
+    spec = {"type": "neural", "params": params, "smoothing": {"maxit": wl.smoothing[0], "omega": wl.smoothing[1]}}
+    strat = harness.CoupledStrategy(tol=wl.tol, maxit=wl.maxit, restart=wl.restart,
+                                    inner_iterations=wl.inner_iterations, three_d=spec)
+    solver = harness.CoupledSolver(wl.systems, strat)
+    flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    reps = None
+    for _ in range(args.warmup):
+        reps = solver.solve()
+    iters = [reps[i].iterations for i in range(len(wl.systems))]
+    conv = [reps[i].converged for i in range(len(wl.systems))]
+    rel = [reps[i].rel_residual for i in range(len(wl.systems))]
+
+    ms_steps = []
+    l0 = lib.mdp_launch_count()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush_l2(flush)
+            barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            reps = solver.solve()
+            e.record()
+            e.synchronize()
+            ms_steps.append(s.elapsed_time(e))
+    launches = lib.mdp_launch_count() - l0
+    t_local = sum(ms_steps)
+    t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    nsolve = len(wl.systems) * args.steps * world
+    value = nsolve / (t_max * 1e-3)
+
+    # -- preconditioner applies/s (smoothed CNN apply, batched over the workload systems)
+    P = solver.inner
+    p = solver.prob
+    V = p.zeros().normal_()
+    Z = p.zeros()
+    sel = torch.arange(p.nsys, dtype=torch.int32, device="cuda")
+    idx = list(range(p.nsys))
+    for _ in range(3):
+        P.apply_device(V, Z, sel, idx)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    na = 20
+    s.record()
+    for _ in range(na):
+        P.apply_device(V, Z, sel, idx)
+    e.record()
+    e.synchronize()
+    applies_per_s = na * p.nsys / (s.elapsed_time(e) * 1e-3)
+
+    out = None
+    if rank == 0:
+        pk = peaks()
+        # -- dominant kernel roofline: tcgen05 conv layers at the workload size
+        n = p.n
+        layers = conv_layer_times(n)
+        per_fwd = {k: v["ms"] for k, v in layers.items()}
+        dom = max(per_fwd, key=per_fwd.get)
+        tf32 = measure_tf32_peak()
+        L = layers[dom]
+        spmv_ms, spmv_bytes = spmv_roofline(solver)
+        # -- e2e through the drop-in API with host buffers
+        e2e_ms, h2d, d2h = e2e_steps(wl, strat, args.steps)
+        line = {
+            "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 system / tf32 CNN",
+            "data": "synthetic (seeded BASELINE graphs, perturbed random-init CNN)",
+            "config": {"workload": args.workload, **wl.meta, "systems_per_gpu": len(wl.systems),
+                       "restart": wl.restart, "rtol": wl.tol, "maxit": wl.maxit,
+                       "inner_iterations": wl.inner_iterations, "smoothing": list(wl.smoothing),
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "iterations": iters, "converged": conv, "rel_residual": rel,
+            "applies_per_s": applies_per_s,
+            "roofline": {"bound": "tensor", "kernel": f"conv3_tc_kernel ({dom}, S={L['S']})",
+                         "achieved": L["tflops"], "peak": tf32, "unit": "TFLOP/s",
+                         "frac": L["tflops"] / tf32, "traffic": None,
+                         "peak_note": "cuBLAS TF32 8192^3 measured in this run",
+                         "frac_of_bf16_measured_over_2": L["tflops"] / (pk["bf16_tflops"] / 2)},
+            "conv_layers": layers,
+            "roofline_spmv": {"bound": "hbm", "kernel": "coupled SpMV (stencil+Pi)",
+                              "achieved": spmv_bytes / (spmv_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"],
+                              "unit": "GB/s", "frac": spmv_bytes / (spmv_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                              "note": "L2-resident at this size" if spmv_bytes < 2 * 126e6 else ""},
+            "e2e": {"value": len(wl.systems) / (e2e_ms * 1e-3), "unit": "solves/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.workload, wl, iters)
+        out = line
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+def e2e_steps(wl, strat, steps):
+    """Drop-in API: harness.solve_coupled(system(s), strategy) from host objects, host results."""
+    import torch
+    from paper_2505_08491_b200 import harness
+    systems = wl.systems if len(wl.systems) > 1 else wl.systems[0]
+    harness.solve_coupled(systems, strat)  # warm caches (weights upload is cached per params object)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = harness.solve_coupled(systems, strat)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    n = sum(s.n3 + s.n1 for s in wl.systems)
+    from paper_2505_08491_b200.assembly import DeviceProblem
+    desc_bytes = sum(t.numel() * t.element_size() for t in DeviceProblem(wl.systems)._t.values())
+    h2d = desc_bytes + 8 * n + 8 * sum(s.n3 for s in wl.systems)
+    d2h = 8 * n
+    return ms, h2d, d2h
+
+
+def cpu_baseline(name, wl, gpu_iters, sample_iters=3):
+    import oracle
+    try:
+        osys = oracle_system(name)
+    except ValueError:
+        return {"value": None, "unit": "solves/s", "cores": len(os.sched_getaffinity(0)), "kind": "port",
+                "sample": "no oracle builder for this workload"}
+    spec = {"type": "neural", "params": oracle.noisy_params(wl.cnn_seed), "smoothing": wl.smoothing}
+    st = oracle.CoupledStrategy(tol=wl.tol, maxit=sample_iters, restart=wl.restart,
+                                inner_iterations=wl.inner_iterations, three_d=spec)
+    t0 = time.perf_counter()
+    oracle.solve_coupled(osys, st)
+    dt = time.perf_counter() - t0
+    full = max(gpu_iters)
+    return {"value": 1.0 / (dt / sample_iters * full), "unit": "solves/s", "cores": len(os.sched_getaffinity(0)),
+            "kind": "port", "sample": f"{sample_iters} outer iterations of the oracle coupled solve "
+                                      f"({dt:.1f} s), extrapolated to the {full} iterations of the full solve"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--maxit", type=int, default=0)
+    ap.add_argument("--ref-iters", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,227 @@
+/*
+ * mdp_b200.h -- C ABI of the B200 (sm_100a) hot path of the neural-
+ * preconditioned FGMRES solve for coupled 3D-1D systems (arXiv 2505.08491,
+ * reference package `mdprec` at /root/reference/pkg/src/mdprec).
+ *
+ * Conventions
+ *   - Every pointer in a call or descriptor is DEVICE memory unless marked
+ *     [host].  Callers own all memory; kernels never allocate.
+ *   - Every function returns 0 on success, MDP_EINVAL on a bad argument, or
+ *     MDP_ECUDA on a CUDA launch/runtime error; mdp_last_error() describes it
+ *     (thread-local).
+ *   - `stream` is a cudaStream_t passed as void*.
+ *   - Batched calls act on `nsel` systems listed in `sel` ([nsel] int32,
+ *     device); sel == NULL means systems 0..nsel-1.  Full vectors of system s
+ *     start at s*ld (3D part [0,n^3), 1D part [n^3, n^3+n1[s]), zero padding
+ *     up to ld).
+ *   - All system arithmetic is float64; the CNN computes in float32 with
+ *     TF32 tensor-core products (tcgen05) and float32 accumulation.
+ *
+ * Each entry point names the reference interface it replaces.
+ */
+#ifndef MDP_B200_H
+#define MDP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDP_OK 0
+#define MDP_EINVAL 1001
+#define MDP_ECUDA 1002
+#define MDP_EPIVOT 1003
+
+/* ------------------------------------------------------------------ */
+/* Coupled problem descriptor (batched over systems that share the grid).
+ * Built on the host by paper_2505_08491_b200.assembly from the index sets
+ * of assemble_coupled_system (assembly.py:306-348).                      */
+typedef struct mdp_problem {
+  int32_t n;            /* grid points per edge (geometry.py:27-43)        */
+  int32_t nsys;         /* systems in the batch                             */
+  int32_t bc3d;         /* 0: Neumann (reference), 1: homogeneous Dirichlet */
+  int32_t pad0;
+  int64_t ld;           /* per-system stride of full vectors                */
+  double h, k_omega, sigma_omega;
+  const double* wc;     /* [nsys] coupling weight w (assembly.py:48-51)     */
+  const int32_t* n1;    /* [nsys] 1D unknowns                               */
+  /* quadrature rows q (2 per 1D element, assembly.py:218-222), global ids */
+  const int32_t* q_start;  /* [nsys+1]                                       */
+  const int32_t* t_ptr;    /* [Qtot+1] row pointers of Pi = T (CSR)          */
+  const int32_t* t_col;    /* local 3D node                                  */
+  const double* t_val;
+  const int32_t* psi_col;  /* [2*Qtot] local 1D node, -1 if Dirichlet (D)    */
+  const double* psi_val;   /* [2*Qtot]                                       */
+  const double* wq;        /* [Qtot] Gauss weights L_e/2 (W)                 */
+  /* Pi^T as a pull over the touched (free) 3D nodes                        */
+  const int32_t* u_start;  /* [nsys+1]                                       */
+  const int32_t* u_node;   /* [Utot] local 3D node                           */
+  const int32_t* u_ptr;    /* [Utot+1]                                       */
+  const int32_t* u_q;      /* global quadrature row                          */
+  const double* u_val;
+  /* 1D rows: K11 after elimination (CSR) and D Psi^T W-free pull          */
+  const int32_t* r1_start; /* [nsys+1] global 1D row offsets                 */
+  const int32_t* k_ptr;    /* [R1tot+1]                                      */
+  const int32_t* k_col;    /* local 1D node                                  */
+  const double* k_val;
+  const int32_t* p_ptr;    /* [R1tot+1] Psi^T rows (empty on Dirichlet rows) */
+  const int32_t* p_q;      /* global quadrature row                          */
+  const double* p_val;
+  const double* diag_c;    /* [nsys*ld] diag(C) for Jacobi (or NULL)        */
+  int32_t qmax, umax, r1max, pad1; /* per-system maxima (launch shapes)      */
+} mdp_problem;
+
+/* y = A x, A = [K00 + w M00, w M01; w M10, K11 + w M11]
+ * replaces full_operator(s) @ x (assembly.py:370-374) via krylov.spmv
+ * (krylov.py:64-69).  s_work: [Qtot] scratch. */
+int mdp_coupled_spmv(const mdp_problem* p, int32_t nsel, const int32_t* sel,
+                     const double* x, double* y, double* s_work, void* stream);
+
+/* y3 = C x3, C = K00 + w M00; replaces reduced_operator(s) @ x
+ * (assembly.py:351-353).  x3/y3 use stride p->ld. */
+int mdp_reduced_spmv(const mdp_problem* p, int32_t nsel, const int32_t* sel,
+                     const double* x3, double* y3, double* s_work, void* stream);
+
+/* Stencil part only: y3 = K00 x3 (assembly.py:122-125, Kronecker form). */
+int mdp_stencil_apply(const mdp_problem* p, int32_t nsel, const int32_t* sel,
+                      const double* x3, int64_t ldx, double* y3, int64_t ldy, void* stream);
+
+/* Pi gather: s_q = W_q ( (T x3)_q - (Psi D x1)_q ); x3 or x1 may be NULL.
+ * Replaces the T @ x3 product inside M00/M01 (assembly.py:324-326). */
+int mdp_pi_gather(const mdp_problem* p, int32_t nsel, const int32_t* sel,
+                  const double* x3, const double* x1, int64_t ld, double* s, void* stream);
+
+/* Pi^T scatter (as a deterministic pull): y3[u] += alpha*w_s * (T^T s)[u].
+ * Replaces T.T @ v (assembly.py:324-326). */
+int mdp_pi_scatter(const mdp_problem* p, int32_t nsel, const int32_t* sel,
+                   const double* s, double alpha, double* y3, int64_t ld, void* stream);
+
+/* Weighted Jacobi sweep on C, fused: x_out = x + omega (r - C x) / diag(C),
+ * replaces krylov.jacobi_smooth (krylov.py:290-299).  x may be NULL (x=0,
+ * no SpMV).  tmp: [nsys*ld] scratch. */
+int mdp_jacobi_sweep(const mdp_problem* p, int32_t nsel, const int32_t* sel,
+                     const double* r, const double* x, double* x_out, double omega,
+                     double* tmp, double* s_work, void* stream);
+
+/* Distance of every grid node to the nearest of nseg segments
+ * seg[e] = (ax, ay, az, bx, by, bz); replaces geometry.distance_field
+ * (geometry.py:293-303), the CNN's second input channel. */
+int mdp_distance_field(int32_t n, const double* seg, int32_t nseg, double* out, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* ILU(0) of the 1D block A11 (krylov.py:188-284).                       */
+
+/* [host] In-place ILU(0) on a sorted CSR matrix; returns -1 on success or
+ * the zero-pivot row (krylov.py:188-216).  diag_pos [n] must be filled. */
+int64_t mdp_ilu0_factor_host(int64_t n, const int64_t* indptr, const int64_t* indices,
+                             double* data, const int64_t* diag_pos);
+
+/* [host] Level schedule of the forward (L) and backward (U) sweeps:
+ * fills perm_f/perm_b [n] and lev_f/lev_b [n+1]; returns number of levels
+ * through nlev_f/nlev_b. */
+int mdp_ilu0_levels_host(int64_t n, const int64_t* indptr, const int64_t* indices,
+                         const int64_t* diag_pos, int32_t* perm_f, int32_t* lev_f,
+                         int32_t* nlev_f, int32_t* perm_b, int32_t* lev_b, int32_t* nlev_b);
+
+typedef struct mdp_ilu {
+  int32_t nsys, lev_stride; /* level arrays are [nsys][lev_stride]       */
+  const int32_t* row_start;  /* [nsys+1] global row offset                 */
+  const int32_t* ptr;        /* [Rtot+1] global CSR pointers               */
+  const int32_t* col;        /* local column                               */
+  const double* val;         /* combined L\U factor                        */
+  const int32_t* diag;       /* [Rtot] global position of the diagonal     */
+  const int32_t* lev_f;      /* level boundaries (local row counts)        */
+  const int32_t* perm_f;     /* [Rtot] local rows ordered by level         */
+  const int32_t* lev_b;
+  const int32_t* perm_b;
+  const int32_t* nlev_f;     /* [nsys]                                     */
+  const int32_t* nlev_b;     /* [nsys]                                     */
+} mdp_ilu;
+
+/* z1 = (LU)^-1 r1, bitwise equal to krylov.ilu0_apply (krylov.py:219-233,
+ * 270-276).  r/z point at the 1D parts; stride ld. */
+int mdp_ilu0_apply(const mdp_ilu* f, int32_t nsel, const int32_t* sel,
+                   const double* r, double* z, int64_t ld, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* Krylov vector kernels (krylov.py:88-182).  V is [nsys][kmax+1][ld].   */
+
+/* Fused Arnoldi orthogonalisation of w against V[0..nv[s]) (CGS2, two
+ * classical passes = MGS-equivalent stability), replaces the MGS loop
+ * krylov.py:138-141.  Writes hcol[s][0..kmax] = projection coefficients,
+ * hcol[s][kmax+1] = ||w_final||, and V[s][nv[s]] = w_final/||w_final||
+ * (vnext, also copied to vcur when non-NULL).  work: scratch of
+ * mdp_arnoldi_work_bytes(). */
+size_t mdp_arnoldi_work_bytes(int32_t nsel, int32_t kmax, int64_t n);
+int mdp_arnoldi(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
+                const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n,
+                double* hcol, double* vcur, int64_t ldc, void* work, void* stream);
+
+/* out[i] = ||x_s||_2 for the selected systems (two-stage deterministic). */
+int mdp_norms(int32_t nsel, const int32_t* sel, const double* x, int64_t ldx, int64_t n,
+              double* out, void* work, void* stream);
+
+/* y_s = alpha_s * x_s  (alpha_s = num[i]/den[i] when den != NULL: exact
+ * division like the reference's w / h_next). */
+int mdp_scale(int32_t nsel, const int32_t* sel, const double* x, int64_t ldx,
+              const double* num, const double* den, double* y, int64_t ldy, int64_t n,
+              void* stream);
+
+/* x_s += sum_{k<cnt[i]} Z_s[k] * y[i][k]  (krylov.py:168-172). */
+int mdp_basis_update(int32_t nsel, const int32_t* sel, double* x, int64_t ldx, const double* Z,
+                     int64_t ldz_sys, int64_t ldz_vec, const int32_t* cnt, const double* y,
+                     int32_t ystride, int64_t n, void* stream);
+
+/* r = b - y and rn[i] = ||r||  (krylov.py:110-111, 173-174). */
+int mdp_residual(int32_t nsel, const int32_t* sel, const double* b, const double* y, double* r,
+                 int64_t ld, int64_t n, double* rn, void* work, void* stream);
+
+/* y = a*x + b*y elementwise over n for all selected systems. */
+int mdp_axpby(int32_t nsel, const int32_t* sel, double a, const double* x, double b, double* y,
+              int64_t ld, int64_t n, void* stream);
+
+/* dst[dst_off[i]] <- src (per-system gather/scatter of one vector). */
+int mdp_copy_vec(int32_t nsel, const int32_t* sel, const double* src, int64_t lds,
+                 double* dst, int64_t ldd, const int32_t* dst_slot, int64_t slot_stride,
+                 int64_t n, void* stream);
+
+/* ------------------------------------------------------------------ */
+/* CNN preconditioner (neural.py:423-472, training.py:290-338).          */
+
+typedef struct mdp_unet {
+  int32_t n;        /* spatial size (points per edge)                      */
+  int32_t path;     /* 0: tcgen05 TF32 implicit GEMM, 1: CUDA-core FP32 check path */
+  const float* w[11];  /* packed weights, ARCHITECTURE order */
+  const float* b[11];  /* biases (NULL where the layer has none)           */
+} mdp_unet;
+
+size_t mdp_unet_workspace_bytes(int32_t n, int32_t nb, int32_t path);
+
+/* z_s = scale_i * U([r_s * inv_i | d_s]) for the nb selected systems,
+ * where inv_i = 1/||r_s|| (1 when zero) and scale_i = ||r_s||; rnorm [nb]
+ * holds ||r_s||.  Replaces apply_neural / apply_batched's forward
+ * (training.py:312-319, 331-338).  r, z: stride ld; dist: stride ldd. */
+int mdp_unet_apply(const mdp_unet* net, int32_t nb, const int32_t* sel, const double* r,
+                   int64_t ld, const double* rnorm, const double* dist, int64_t ldd, double* z,
+                   int64_t ldz, void* workspace, size_t ws_bytes, void* stream);
+
+/* Single-layer entry points used by the parity tests (float32 C4-blocked
+ * activations [b][C/4][S][S][S][4]). */
+int mdp_conv3_layer(int32_t path, int32_t nb, int32_t S, int32_t cin, int32_t cout,
+                    const float* in, int32_t in_cq, int32_t in_q0, const float* w, const float* bias,
+                    int32_t relu, float* out, int32_t out_cq, int32_t out_q0, int32_t pool,
+                    void* stream);
+
+/* ------------------------------------------------------------------ */
+const char* mdp_last_error(void);
+int mdp_version(void);
+/* Number of kernels this library has launched in the process. */
+long long mdp_launch_count(void);
+int mdp_device_sm_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDP_B200_H */

@@ -1,0 +1,43 @@
+// Shared declarations of the U-Net apply (unet.cu) and the tcgen05 conv
+// kernel (unet_tc.cu).
+#pragma once
+#include "common.cuh"
+
+namespace mdp {
+
+struct UnetPlan {
+  int n, m, q;
+  size_t o_xin, o_a1, o_c1, o_c2, o_p2, o_bt, o_d2, o_d1, o_e2, o_e3;
+  size_t bytes;
+};
+UnetPlan unet_plan(int n, int nb, int path);
+
+enum Epilogue { EPI_STORE = 0, EPI_POOL = 1, EPI_HEAD = 2 };
+
+struct HeadArgs {  // dec1 -> head1 -> head2 -> scale (EPI_HEAD)
+  const float* w1;
+  const float* b1;
+  const float* w2;
+  const float* b2;
+  const int32_t* sel;
+  const double* rnorm;
+  double* z;
+  int64_t ldz;
+};
+
+// 3x3x3 same-padding conv on tensor cores (tcgen05 kind::tf32).
+// w packed by paper_2505_08491_b200.neural.pack_tc.
+int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int in_q0, const float* w,
+             const float* bias, int relu, float4* out, int out_cq, int out_q0, int epi, const HeadArgs* head,
+             cudaStream_t st);
+
+__device__ __forceinline__ float tf32_round(float f) {
+  uint32_t u;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(f));
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ float4 tf32_round4(float4 v) {
+  return make_float4(tf32_round(v.x), tf32_round(v.y), tf32_round(v.z), tf32_round(v.w));
+}
+
+}  // namespace mdp

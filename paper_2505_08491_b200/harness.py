@@ -1,0 +1,152 @@
+"""Coupled neural-preconditioned solve on the device (the north-star path).
+
+``solve_coupled`` reproduces ``harness.solve_coupled`` (harness.py:342-398):
+outer FGMRES on the block operator with the block right preconditioner
+
+    z1 = ILU0(A11)^-1 r1
+    z0 = FGMRES(C, P3, r0 - w M01 z1, restart=m, tol=1e-300, maxit=m)
+
+and the eliminated Dirichlet values reimposed on u1d.  Given a list of
+systems on one grid it solves them concurrently (the paper's multi-query
+setting): every kernel runs once per step over all systems still
+iterating, each system keeping its own FGMRES state.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _ext
+from .assembly import CoupledSystem, DeviceProblem, full_rhs, one_d_operator
+from .geometry import DistanceField, distance_field_device
+from .krylov import DeviceIlu, FgmresEngine, IluPreconditioner, SolveReport, ilu0
+from .neural import PATH_TCGEN05, UNetParams, device_net, load_checkpoint
+from .operators import CoupledOperator, CouplingOps, ReducedOperator
+from .training import BatchedNeural, NeuralPreconditioner
+
+
+@dataclass
+class CoupledStrategy:
+    """harness.py:324-339.  ``one_d`` must be 'ilu0' (the reference default)."""
+
+    tol: float = 1e-15
+    maxit: int = 2000
+    restart: int = 20
+    inner_iterations: int = 3
+    one_d: str = "ilu0"
+    three_d: object = None
+
+
+def build_preconditioner(spec: dict, grid, C, dfield: DistanceField):
+    """Preconditioner factory (harness.py:204-226) for the device path.
+
+    Supported: 'none' and 'neural' (checkpoint path or in-memory
+    ``params``, optional ``smoothing``/``zero_distance``).  The classical
+    baselines (exact / gmg / 3D ilu0) are outside the hot path.
+    """
+    kind = spec.get("type", "none")
+    if kind == "none":
+        return None
+    if kind == "neural":
+        params = spec.get("params") or load_checkpoint(spec["checkpoint"])
+        sm = spec.get("smoothing")
+        smooth = (sm["maxit"], sm.get("omega", 2.0 / 3.0)) if isinstance(sm, dict) else sm
+        return NeuralPreconditioner(params, dfield, smoothing=smooth, C=C,
+                                    zero_distance=spec.get("zero_distance", False))
+    if kind == "ilu0" and C is not None and C.shape[0] <= 8000:
+        return IluPreconditioner(C)
+    raise ValueError(f"preconditioner type {kind!r} is not on the device hot path")
+
+
+def mesh_distance(system: CoupledSystem):
+    """CNN distance channel from the refined mesh (harness.py:401-406), on the device."""
+    return distance_field_device(system.graph_mesh.coords, system.graph_mesh.elements, system.grid)
+
+
+class CoupledSolver:
+    """Device state for repeated coupled solves of a batch of systems."""
+
+    def __init__(self, systems, strategy: CoupledStrategy, path: int = PATH_TCGEN05):
+        import torch
+        if strategy.one_d != "ilu0":
+            raise ValueError("the device path implements the one_d='ilu0' strategy")
+        self.systems = list(systems)
+        self.st = strategy
+        self.prob = DeviceProblem(self.systems)
+        p = self.prob
+        self.A = CoupledOperator(p)
+        self.C = ReducedOperator(p)
+        self.cpl = CouplingOps(p)
+        self.ilu = DeviceIlu([ilu0(one_d_operator(s)) for s in self.systems])
+        self.lib = _ext.lib()
+        spec = strategy.three_d or {"type": "none"}
+        kind = spec.get("type", "none")
+        self.inner = None
+        if kind == "neural":
+            params = spec.get("params")
+            if params is None:
+                params = load_checkpoint(spec["checkpoint"])
+            if not isinstance(params, UNetParams):
+                raise TypeError("neural spec needs UNetParams")
+            sm = spec.get("smoothing")
+            smooth = (sm["maxit"], sm.get("omega", 2.0 / 3.0)) if isinstance(sm, dict) else sm
+            dists = torch.stack([mesh_distance(s) for s in self.systems])
+            self.inner = BatchedNeural(device_net(params, spec.get("path", path)), dists, p.n, p.ld, p.nsys,
+                                       C=self.C, smoothing=smooth,
+                                       zero_distance=spec.get("zero_distance", False))
+        elif kind != "none":
+            raise ValueError(f"inner preconditioner {kind!r} is not on the device hot path")
+        self.outer = FgmresEngine(p.nsys, p.n3 + p.n1max, p.ld, strategy.restart)
+        self.inner_eng = FgmresEngine(p.nsys, p.n3, p.ld, strategy.inner_iterations)
+        self.b3 = p.zeros()
+        self.F = p.pack([full_rhs(s) for s in self.systems])
+
+    def _block_precond(self, V, Z, sel, idx):
+        p = self.prob
+        m = int(sel.numel())
+        n3 = p.n3
+        # z1 = ILU(r1)   (krylov.py:270-276 via harness.py:390)
+        _ext.check(self.lib.mdp_ilu0_apply(self.ilu.desc, m, sel.data_ptr(), V.data_ptr() + 8 * n3,
+                                           Z.data_ptr() + 8 * n3, p.ld, _ext.stream()))
+        # r0 - w M01 z1  (harness.py:391)
+        _ext.check(self.lib.mdp_copy_vec(m, sel.data_ptr(), V.data_ptr(), p.ld, self.b3.data_ptr(), p.ld, None, 0,
+                                         n3, _ext.stream()))
+        self.cpl.minus_w_m01(Z, self.b3, sel)
+        # z0 = 3-step inner FGMRES on C (harness.py:385-387)
+        m_in = self.st.inner_iterations
+        P = self.inner.apply_device if self.inner is not None else None
+        self.inner_eng.solve(self.C.matvec, P, self.b3, tol=1e-300, maxit=m_in, systems=idx,
+                             final_residual=False)
+        _ext.check(self.lib.mdp_copy_vec(m, sel.data_ptr(), self.inner_eng.x.data_ptr(), p.ld, Z.data_ptr(), p.ld,
+                                         None, 0, n3, _ext.stream()))
+
+    def solve(self, F=None):
+        """Outer FGMRES (harness.py:394-395); returns per-system reports, x left on device."""
+        st = self.st
+        return self.outer.solve(self.A.matvec, self._block_precond, self.F if F is None else F,
+                                tol=st.tol, maxit=st.maxit)
+
+    def solution(self):
+        out = []
+        X = self.prob.unpack(self.outer.x)
+        for s, x in zip(self.systems, X):
+            u3, u1 = x[:s.n3], x[s.n3:].copy()
+            u1[list(s.dirichlet_nodes)] = 1.0  # harness.py:396-397
+            out.append((u3, u1))
+        return out
+
+
+def solve_coupled(system, strategy: CoupledStrategy):
+    """Drop-in ``harness.solve_coupled``: (u3d, u1d, SolveReport).
+
+    A list of systems on one grid is solved concurrently and a list of
+    triples is returned.
+    """
+    many = isinstance(system, (list, tuple))
+    systems = list(system) if many else [system]
+    solver = CoupledSolver(systems, strategy)
+    reps = solver.solve()
+    res = [(u3, u1, reps[i]) for i, (u3, u1) in enumerate(solver.solution())]
+    return res if many else res[0]

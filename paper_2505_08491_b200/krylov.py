@@ -1,0 +1,507 @@
+"""Flexible GMRES on the device, batched over independent systems.
+
+Reproduces ``mdprec.krylov.fgmres`` (krylov.py:88-182) control flow
+literally: breakdown attempts count as iterations,
+an Arnoldi breakdown (hypot(H_jj, h_next) < 1e-14) ends the cycle without
+advancing j, a lucky breakdown (h_next < 1e-14) ends it after, the Givens
+estimate only ends a cycle early, and convergence is declared solely from
+the true residual ||b - A x|| / ||r0|| at cycle boundaries.
+
+The vectors (V, Z, x, r, w) live in HBM as [nsys][k][ld] float64; the
+orthogonalisation is the fused CGS2 kernel (mdp_arnoldi); the small
+Hessenberg / Givens / back-substitution work runs on the host from one
+device->host read of the new Hessenberg column per Arnoldi step for all
+systems at once.  Each system keeps its own j, cycle, iteration count and
+convergence state, so a batched solve reproduces every system's serial
+solve (multi-query setting, paper section 5.7).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _ext
+
+BREAKDOWN_TOL = 1e-14  # krylov.py:28
+
+
+@dataclass
+class SolveReport:
+    """Outcome of one preconditioned solve (krylov.py:31-41)."""
+
+    iterations: int
+    converged: bool
+    residual_history: list
+    rel_residual: float
+    wall_time: float
+    time_per_iter: float
+    breakdowns: int = 0
+
+
+class Preconditioner:
+    """Apply contract ``z = P(r)`` (krylov.py:44-51).
+
+    Device preconditioners additionally implement ``apply_device(V, Z,
+    sel)`` on ``(nsys, ld)`` float64 storages.
+    """
+
+    def apply(self, r):
+        raise NotImplementedError
+
+    def __call__(self, r):
+        return self.apply(r)
+
+
+def spmv(A, x):
+    """CSR / device-operator product with a dimension check (krylov.py:64-69)."""
+    x = np.asarray(x)
+    if A.shape[1] != x.shape[0]:
+        raise ValueError(f"dimension mismatch: {A.shape} @ {x.shape}")
+    return A @ x
+
+
+class _State:
+    __slots__ = ("j", "iters", "brk", "conv", "r0", "hist", "H", "cs", "sn", "g", "done", "rel", "beta",
+                 "t0", "wall")
+
+    def __init__(self, k):
+        self.j = 0
+        self.iters = 0
+        self.brk = 0
+        self.conv = False
+        self.done = False
+        self.r0 = 0.0
+        self.hist = [1.0]
+        self.H = np.zeros((k + 1, k))
+        self.cs = np.zeros(k)
+        self.sn = np.zeros(k)
+        self.g = np.zeros(k + 1)
+        self.rel = 0.0
+        self.beta = 0.0
+
+
+class FgmresEngine:
+    """Workspace + driver for batched right-preconditioned FGMRES(k).
+
+    ``A(X, Y, sel)`` and ``P(V, Z, sel, idx)`` act on (nsys, ld) float64
+    CUDA storages for the systems listed in the int32 CUDA tensor ``sel``
+    (``idx``: the same list on the host).
+    ``n`` is the active vector length (entries beyond it stay zero).
+    """
+
+    def __init__(self, nsys: int, n: int, ld: int, restart: int, device="cuda"):
+        import torch
+        if restart < 1:
+            raise ValueError("restart must be at least 1")
+        self.lib = _ext.lib()
+        self.nsys, self.n, self.ld, self.k = nsys, n, ld, restart
+        f = dict(dtype=torch.float64, device=device)
+        self.V = torch.zeros((nsys, restart + 1, ld), **f)
+        self.Z = torch.zeros((nsys, restart, ld), **f)
+        self.x = torch.zeros((nsys, ld), **f)
+        self.r = torch.zeros((nsys, ld), **f)
+        self.w = torch.zeros((nsys, ld), **f)
+        self.vcur = torch.zeros((nsys, ld), **f)
+        self.zcur = torch.zeros((nsys, ld), **f)
+        self.tmp = torch.zeros((nsys, ld), **f)
+        self.hcol = torch.zeros((nsys, restart + 2), **f)
+        self.rn = torch.zeros(nsys, **f)
+        self.ybuf = torch.zeros((nsys, restart), **f)
+        self.betad = torch.zeros(nsys, **f)
+        wb = max(self.lib.mdp_arnoldi_work_bytes(nsys, restart, n), 8 * nsys * 1024)
+        self.work = torch.empty(wb // 8 + 1, **f)
+        pin = dict(pin_memory=True)
+        self.h_host = torch.zeros((nsys, restart + 2), dtype=torch.float64, **pin)
+        self.rn_host = torch.zeros(nsys, dtype=torch.float64, **pin)
+        self.y_host = torch.zeros((nsys, restart), dtype=torch.float64, **pin)
+        self.beta_host = torch.zeros(nsys, dtype=torch.float64, **pin)
+        # one pinned staging slot + device copy per upload purpose: a slot is
+        # rewritten only after a stream synchronisation since its last copy
+        self._regions = {}
+        for name in ("all", "start", "arn", "js", "nv", "end", "cnt", "res"):
+            self._regions[name] = (torch.zeros(nsys, dtype=torch.int32, pin_memory=True),
+                                   torch.zeros(nsys, dtype=torch.int32, device=device))
+
+    # -- small helpers -------------------------------------------------------------
+    def _upload(self, name, values):
+        """Small int32 list -> device through its dedicated pinned slot."""
+        import torch
+        host, dev = self._regions[name]
+        m = len(values)
+        host[:m] = torch.as_tensor(np.asarray(values, dtype=np.int32))
+        dev[:m].copy_(host[:m], non_blocking=True)
+        return dev[:m]
+
+    def _sync_read(self, dev, host, m):
+        import torch
+        host[:m].copy_(dev[:m], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return host[:m].numpy()
+
+    def _residual(self, A, b, sel, m):
+        """r = b - A x for the selected systems; returns ||r|| on the host."""
+        A(self.x, self.tmp, sel)
+        _ext.check(self.lib.mdp_residual(m, sel.data_ptr(), b.data_ptr(), self.tmp.data_ptr(),
+                                         self.r.data_ptr(), self.ld, self.n, self.rn.data_ptr(),
+                                         self.work.data_ptr(), _ext.stream()))
+        return self._sync_read(self.rn, self.rn_host, m).copy()
+
+    # -- the solve -----------------------------------------------------------------
+    def solve(self, A, P, b, tol: float = 1e-6, maxit: int = 1000, x0=None, systems=None,
+              final_residual: bool = True):
+        """Solve A x = b for the listed systems (default all); returns reports.
+
+        ``b`` is an (nsys, ld) storage; ``x0`` an optional storage.  The
+        solution is left in ``self.x``.  ``final_residual=False`` skips the
+        last cycle's true-residual computation when no further cycle can
+        follow (inner solves whose report is discarded, harness.py:385-387);
+        the returned x is unaffected.
+        """
+        import torch
+        if tol <= 0:
+            raise ValueError("tol must be positive")
+        systems = list(range(self.nsys)) if systems is None else list(systems)
+        k = self.k
+        t_start = time.perf_counter()
+        st = {s: _State(k) for s in systems}
+        sel_all = self._upload("all", systems)
+        m = len(systems)
+        if x0 is None:
+            # r = b - A(0) = b exactly; skip the SpMV of a zero vector
+            self.x.index_fill_(0, sel_all.long(), 0.0)
+            self.r.index_copy_(0, sel_all.long(), b.index_select(0, sel_all.long()))
+            _ext.check(self.lib.mdp_norms(m, sel_all.data_ptr(), self.r.data_ptr(), self.ld, self.n,
+                                          self.rn.data_ptr(), self.work.data_ptr(), _ext.stream()))
+            rn = self._sync_read(self.rn, self.rn_host, m).copy()
+        else:
+            self.x.index_copy_(0, sel_all.long(), x0.index_select(0, sel_all.long()))
+            rn = self._residual(A, b, sel_all, m)
+        starting = []
+        for i, s in enumerate(systems):
+            S = st[s]
+            S.r0 = float(rn[i])
+            S.beta = S.r0
+            if S.r0 == 0.0:
+                S.done, S.conv, S.hist, S.rel = True, True, [0.0], 0.0
+            else:
+                starting.append(s)
+        arn = []          # systems currently inside a cycle
+        while True:
+            # ---- cycle starts (krylov.py:123-134)
+            if starting:
+                go = []
+                for s in starting:
+                    S = st[s]
+                    if S.iters >= maxit:
+                        self._finish(S)
+                        continue
+                    if S.beta / S.r0 <= tol:
+                        S.conv = True
+                        self._finish(S)
+                        continue
+                    go.append(s)
+                    S.H[:] = 0.0
+                    S.cs[:] = 0.0
+                    S.sn[:] = 0.0
+                    S.g[:] = 0.0
+                    S.g[0] = S.beta
+                    S.j = 0
+                if go:
+                    sel = self._upload("start", go)
+                    self.beta_host[:len(go)] = torch.as_tensor(np.array([st[s].beta for s in go], dtype=np.float64))
+                    self.betad[:len(go)].copy_(self.beta_host[:len(go)], non_blocking=True)
+                    # V[0] = r / beta (exact division) and the current vector
+                    V0 = self.V[:, 0, :]
+                    _ext.check(self.lib.mdp_scale(len(go), sel.data_ptr(), self.r.data_ptr(), self.ld, None,
+                                                  self.betad.data_ptr(), V0.data_ptr(), (k + 1) * self.ld,
+                                                  self.n, _ext.stream()))
+                    _ext.check(self.lib.mdp_copy_vec(len(go), sel.data_ptr(), V0.data_ptr(), (k + 1) * self.ld,
+                                                     self.vcur.data_ptr(), self.ld, None, 0, self.n,
+                                                     _ext.stream()))
+                    arn.extend(go)
+                starting = []
+            if not arn:
+                break
+            arn.sort()
+            # ---- one Arnoldi step for every system inside a cycle (krylov.py:135-167)
+            js = [st[s].j for s in arn]
+            sel = self._upload("arn", arn)
+            jd = self._upload("js", js)
+            nv = self._upload("nv", [j + 1 for j in js])
+            ma = len(arn)
+            if P is None:
+                _ext.check(self.lib.mdp_copy_vec(ma, sel.data_ptr(), self.vcur.data_ptr(), self.ld,
+                                                 self.zcur.data_ptr(), self.ld, None, 0, self.n, _ext.stream()))
+            else:
+                P(self.vcur, self.zcur, sel, arn)
+            # Z[j] = z
+            _ext.check(self.lib.mdp_copy_vec(ma, sel.data_ptr(), self.zcur.data_ptr(), self.ld,
+                                             self.Z.data_ptr(), k * self.ld, jd.data_ptr(), self.ld, self.n,
+                                             _ext.stream()))
+            A(self.zcur, self.w, sel)
+            # nv = j + 1 projections; V[j+1] = w / ||w|| written on device (also vcur)
+            _ext.check(self.lib.mdp_arnoldi(ma, sel.data_ptr(), self.V.data_ptr(), (k + 1) * self.ld, self.ld,
+                                            nv.data_ptr(), k, self.w.data_ptr(), self.ld, self.n,
+                                            self.hcol.data_ptr(), self.vcur.data_ptr(), self.ld,
+                                            self.work.data_ptr(), _ext.stream()))
+            hc = self._sync_read(self.hcol, self.h_host, ma)
+            ending = []
+            for i, s in enumerate(arn):
+                S = st[s]
+                j = S.j
+                H, cs, sn, g = S.H, S.cs, S.sn, S.g
+                H[:j + 1, j] = hc[i, :j + 1]
+                h_next = float(hc[i, k + 1])
+                for ii in range(j):
+                    t = cs[ii] * H[ii, j] + sn[ii] * H[ii + 1, j]
+                    H[ii + 1, j] = -sn[ii] * H[ii, j] + cs[ii] * H[ii + 1, j]
+                    H[ii, j] = t
+                denom = np.hypot(H[j, j], h_next)
+                if denom < BREAKDOWN_TOL:
+                    S.iters += 1
+                    S.hist.append(S.hist[-1])
+                    S.brk += 1
+                    ending.append(s)
+                    continue
+                cs[j], sn[j] = H[j, j] / denom, h_next / denom
+                H[j, j] = denom
+                g[j + 1] = -sn[j] * g[j]
+                g[j] = cs[j] * g[j]
+                S.iters += 1
+                est = abs(g[j + 1]) / S.r0
+                S.hist.append(est)
+                S.j = j + 1
+                if h_next < BREAKDOWN_TOL:
+                    S.brk += 1
+                    ending.append(s)
+                elif est <= tol or S.j >= k or S.iters >= maxit:
+                    ending.append(s)
+            if ending:
+                arn = [s for s in arn if s not in set(ending)]
+                self._end_cycles(A, b, st, ending, tol, maxit, final_residual)
+                starting = [s for s in ending if not st[s].done]
+        wall = time.perf_counter() - t_start
+        reports = {}
+        for s in systems:
+            S = st[s]
+            reports[s] = SolveReport(S.iters, S.conv, S.hist, S.rel, wall, wall / S.iters if S.iters else 0.0,
+                                     S.brk)
+        return reports
+
+    def _finish(self, S):
+        # krylov.py:177-181: rel = ||b - A x|| / r0 (x unchanged since the last residual)
+        S.rel = float(S.beta / S.r0)
+        S.hist.append(S.rel)
+        S.done = True
+
+    def _end_cycles(self, A, b, st, ending, tol, maxit, final_residual):
+        """x += Z[:j] y, r = b - A x, convergence test (krylov.py:168-175)."""
+        import torch
+        upd = [s for s in ending if st[s].j > 0]
+        if upd:
+            ys = np.zeros((len(upd), self.k))
+            for i, s in enumerate(upd):
+                S = st[s]
+                j = S.j
+                y = np.zeros(j)
+                for ii in range(j - 1, -1, -1):
+                    y[ii] = (S.g[ii] - S.H[ii, ii + 1:j] @ y[ii + 1:j]) / S.H[ii, ii]
+                ys[i, :j] = y
+            sel = self._upload("end", upd)
+            cnt = self._upload("cnt", [st[s].j for s in upd])
+            self.y_host[:len(upd)] = torch.as_tensor(ys)
+            self.ybuf[:len(upd)].copy_(self.y_host[:len(upd)], non_blocking=True)
+            _ext.check(self.lib.mdp_basis_update(len(upd), sel.data_ptr(), self.x.data_ptr(), self.ld,
+                                                 self.Z.data_ptr(), self.k * self.ld, self.ld, cnt.data_ptr(),
+                                                 self.ybuf.data_ptr(), self.k, self.n, _ext.stream()))
+        # systems whose x changed need a new true residual; a breakdown at j=0
+        # leaves x (hence r) unchanged bitwise, so the previous norm stands
+        need = []
+        for s in ending:
+            S = st[s]
+            if S.j == 0:
+                continue
+            if not final_residual and S.iters >= maxit:
+                S.done = True
+                S.rel = float("nan")
+                continue
+            need.append(s)
+        if need:
+            sel = self._upload("res", need)
+            rn = self._residual(A, b, sel, len(need))
+            for i, s in enumerate(need):
+                st[s].beta = float(rn[i])
+        for s in ending:
+            S = st[s]
+            if S.done:
+                continue
+            if S.beta / S.r0 <= tol:
+                S.conv = True
+            if S.conv or S.iters >= maxit:
+                self._finish(S)
+
+
+# ---------------------------------------------------------------------------
+# drop-in host-vector entry point
+
+def _host_apply(op):
+    if sp.issparse(op):
+        return lambda v: op @ v
+    if callable(op):
+        return op
+    raise TypeError("operator must be a sparse matrix, a device operator or a callable")
+
+
+def fgmres(apply_A, precond, b, restart: int = 20, tol: float = 1e-6, maxit: int = 1000, x0=None):
+    """Drop-in ``krylov.fgmres`` (krylov.py:88-182) on the device.
+
+    ``apply_A`` must be a device operator (``full_operator`` /
+    ``reduced_operator`` of this package); ``precond`` is None, a device
+    preconditioner of this package, or any callable / Preconditioner on
+    host vectors (then applied through a host round trip).  Returns
+    ``(x, SolveReport)`` with host numpy x.
+    """
+    import torch
+    if restart < 1:
+        raise ValueError("restart must be at least 1")
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    if precond is not None and not (isinstance(precond, Preconditioner) or callable(precond)):
+        raise TypeError("preconditioner must be None, callable, or Preconditioner")
+    if not hasattr(apply_A, "matvec"):
+        raise TypeError("apply_A must be a device operator (full_operator / reduced_operator)")
+    prob = apply_A.prob
+    b = np.asarray(b, dtype=float)
+    n = b.shape[0]
+    if n != apply_A.shape[0]:
+        raise ValueError(f"dimension mismatch: {apply_A.shape} @ {b.shape}")
+    eng = FgmresEngine(1, n, prob.ld, restart)
+    B = prob.zeros()
+    B[0, :n] = torch.as_tensor(b, device=prob.device)
+    X0 = None
+    if x0 is not None:
+        X0 = prob.zeros()
+        X0[0, :n] = torch.as_tensor(np.asarray(x0, dtype=float), device=prob.device)
+    P = None
+    if precond is not None:
+        if hasattr(precond, "apply_device"):
+            P = precond.apply_device
+        else:
+            fn = precond.apply if isinstance(precond, Preconditioner) else precond
+
+            def P(V, Z, sel, idx, fn=fn):
+                z = np.asarray(fn(V[0, :n].cpu().numpy()), dtype=float)
+                Z[0, :n] = torch.as_tensor(z, device=prob.device)
+
+    rep = eng.solve(apply_A.matvec, P, B, tol=tol, maxit=maxit, x0=X0)[0]
+    return eng.x[0, :n].cpu().numpy(), rep
+
+
+# ---------------------------------------------------------------------------
+# ILU(0) of the 1D block
+
+class IluFactorization:
+    """Host ILU(0) factor (krylov.py:236-267) + device level schedule."""
+
+    def __init__(self, A):
+        A = sp.csr_matrix(A).copy()
+        A.sort_indices()
+        if A.shape[0] != A.shape[1]:
+            raise ValueError("ILU(0) needs a square matrix")
+        n = A.shape[0]
+        ip = A.indptr.astype(np.int64)
+        ix = A.indices.astype(np.int64)
+        dpos = np.full(n, -1, dtype=np.int64)
+        for i in range(n):
+            row = ix[ip[i]:ip[i + 1]]
+            h = np.searchsorted(row, i)
+            if h < len(row) and row[h] == i:
+                dpos[i] = ip[i] + h
+        miss = np.nonzero(dpos < 0)[0]
+        if len(miss):
+            raise ValueError(f"zero pivot: row {miss[0]} has no diagonal entry")
+        data = A.data.astype(float).copy()
+        lib = _ext.load_library()
+        bad = lib.mdp_ilu0_factor_host(n, ip.ctypes.data, ix.ctypes.data, data.ctypes.data, dpos.ctypes.data)
+        if bad >= 0:
+            raise ValueError(f"zero pivot in row {bad} during ILU(0)")
+        self.indptr, self.indices, self.data, self.diag_pos, self.shape = ip, ix, data, dpos, A.shape
+        pf = np.zeros(n, dtype=np.int32)
+        pb = np.zeros(n, dtype=np.int32)
+        lf = np.zeros(n + 1, dtype=np.int32)
+        lb = np.zeros(n + 1, dtype=np.int32)
+        nf = np.zeros(1, dtype=np.int32)
+        nb = np.zeros(1, dtype=np.int32)
+        lib.mdp_ilu0_levels_host(n, ip.ctypes.data, ix.ctypes.data, dpos.ctypes.data, pf.ctypes.data,
+                                 lf.ctypes.data, nf.ctypes.data, pb.ctypes.data, lb.ctypes.data, nb.ctypes.data)
+        self.perm_f, self.lev_f, self.nlev_f = pf, lf, int(nf[0])
+        self.perm_b, self.lev_b, self.nlev_b = pb, lb, int(nb[0])
+
+
+def ilu0(A) -> IluFactorization:
+    return IluFactorization(A)
+
+
+class DeviceIlu:
+    """Batched device sweeps of per-system ILU(0) factors (``mdp_ilu``)."""
+
+    def __init__(self, factors, device="cuda"):
+        import torch
+        nsys = len(factors)
+        rows = [f.shape[0] for f in factors]
+        stride = max(rows) + 1
+        row_start = np.concatenate([[0], np.cumsum(rows)]).astype(np.int32)
+        nnz = [len(f.data) for f in factors]
+        nz_start = np.concatenate([[0], np.cumsum(nnz)])
+        ptr = np.concatenate([f.indptr[:-1] + nz_start[i] for i, f in enumerate(factors)] + [[nz_start[-1]]])
+        col = np.concatenate([f.indices for f in factors])
+        val = np.concatenate([f.data for f in factors])
+        diag = np.concatenate([f.diag_pos + nz_start[i] for i, f in enumerate(factors)])
+        lev_f = np.zeros((nsys, stride), dtype=np.int32)
+        lev_b = np.zeros((nsys, stride), dtype=np.int32)
+        for i, f in enumerate(factors):
+            lev_f[i, :f.nlev_f + 1] = f.lev_f[:f.nlev_f + 1]
+            lev_b[i, :f.nlev_b + 1] = f.lev_b[:f.nlev_b + 1]
+        if max(rows) > 8000:
+            raise ValueError("1D block too large for the single-CTA ILU sweep (shared memory)")
+        T = lambda a, dt=torch.int32: torch.as_tensor(np.ascontiguousarray(a).ravel(), dtype=dt, device=device)  # noqa: E731
+        self._t = dict(row_start=T(row_start), ptr=T(ptr), col=T(col), val=T(val, torch.float64), diag=T(diag),
+                       lev_f=T(lev_f), perm_f=T(np.concatenate([f.perm_f for f in factors])),
+                       lev_b=T(lev_b), perm_b=T(np.concatenate([f.perm_b for f in factors])),
+                       nlev_f=T([f.nlev_f for f in factors]), nlev_b=T([f.nlev_b for f in factors]))
+        d = _ext.MdpIlu()
+        d.nsys, d.lev_stride = nsys, stride
+        for key, t in self._t.items():
+            setattr(d, key, t.data_ptr())
+        self.desc = d
+        self.lib = _ext.lib()
+
+    def apply(self, R, Z, ld, sel=None, nsys=None):
+        cnt = int(sel.numel()) if sel is not None else int(nsys)
+        _ext.check(self.lib.mdp_ilu0_apply(self.desc, cnt, None if sel is None else sel.data_ptr(),
+                                           R.data_ptr(), Z.data_ptr(), ld, _ext.stream()))
+
+
+def ilu0_apply(fact: IluFactorization, r):
+    """Host-vector drop-in for krylov.ilu0_apply (krylov.py:270-276), run on the device."""
+    import torch
+    r = np.asarray(r, dtype=float)
+    if r.shape != (fact.shape[0],):
+        raise ValueError("right-hand side length mismatch")
+    dev = DeviceIlu([fact])
+    R = torch.as_tensor(r, device="cuda").reshape(1, -1)
+    Z = torch.zeros_like(R)
+    dev.apply(R, Z, R.shape[1], nsys=1)
+    return Z[0].cpu().numpy()
+
+
+class IluPreconditioner(Preconditioner):
+    def __init__(self, A):
+        self.fact = ilu0(A)
+
+    def apply(self, r):
+        return ilu0_apply(self.fact, r)

@@ -1,0 +1,166 @@
+"""Preconditioner apply path: ``apply_neural``, ``apply_batched``,
+``NeuralPreconditioner`` (training.py:287-355), on the device.
+
+z = ||r|| U([r/||r|| | d]) with r = 0 -> 0; with ``smoothing=(maxit, omega)``
+the correction is wrapped in weighted-Jacobi pre/post sweeps on C
+(training.py:304-311, krylov.py:290-299), each sweep one fused
+reduced-SpMV + update on the device.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _ext
+from .geometry import DistanceField
+from .krylov import Preconditioner
+from .neural import PATH_TCGEN05, device_net
+
+
+class BatchedNeural:
+    """Neural (+ optional Jacobi) preconditioner over a DeviceProblem batch.
+
+    ``apply_device(V, Z, sel, idx)``: Z_s = P_s(V_s) for the listed systems;
+    V, Z are (nsys, ld) float64 storages, only the 3D part is used.
+    """
+
+    def __init__(self, net, dists, n: int, ld: int, nsys: int, C=None, smoothing=None,
+                 zero_distance: bool = False):
+        import torch
+        self.net, self.n, self.ld, self.nsys = net, n, ld, nsys
+        self.n3 = n ** 3
+        self.C = C
+        self.smoothing = smoothing
+        if smoothing is not None and C is None:
+            raise ValueError("smoothing needs the reduced operator")
+        dev = "cuda"
+        self.D = torch.zeros((nsys, self.n3), dtype=torch.float64, device=dev)
+        if not zero_distance:
+            self.D.copy_(dists)
+        f = dict(dtype=torch.float64, device=dev)
+        self.rn = torch.zeros(nsys, **f)
+        self.work = torch.zeros(4 * 148 * nsys + 1024, **f)
+        if smoothing is not None:
+            self.t1 = torch.zeros((nsys, ld), **f)
+            self.t2 = torch.zeros((nsys, ld), **f)
+            self.rr = torch.zeros((nsys, ld), **f)
+            self.zn = torch.zeros((nsys, ld), **f)
+            self.tmp = torch.zeros((nsys, ld), **f)
+        self.lib = _ext.lib()
+
+    def _net(self, R, Z, sel, m):
+        # ||r|| per system, then the fused pack -> U-Net -> rescale (float64 out)
+        _ext.check(self.lib.mdp_norms(m, sel.data_ptr(), R.data_ptr(), self.ld, self.n3, self.rn.data_ptr(),
+                                      self.work.data_ptr(), _ext.stream()))
+        self.net.apply(self.n, R, self.ld, self.rn, self.D, self.n3, Z, self.ld, sel=sel)
+
+    def apply_device(self, V, Z, sel, idx=None):
+        m = int(sel.numel())
+        if self.smoothing is None:
+            self._net(V, Z, sel, m)
+            return
+        maxit, omega = self.smoothing
+        C = self.C
+        # z = S_J(C, r, 0): first sweep from zero needs no SpMV
+        cur = None
+        bufs = [self.t1, self.t2]
+        for it in range(maxit):
+            out = bufs[it % 2]
+            C.jacobi(V, cur, out, omega, self.tmp, sel)
+            cur = out
+        if cur is None:
+            Z.index_fill_(0, sel.long(), 0.0)
+            cur = Z
+        # rr = r - C z and ||rr||, then zn = U(rr)
+        C.matvec(cur, self.tmp, sel)
+        _ext.check(self.lib.mdp_residual(m, sel.data_ptr(), V.data_ptr(), self.tmp.data_ptr(), self.rr.data_ptr(),
+                                         self.ld, self.n3, self.rn.data_ptr(), self.work.data_ptr(),
+                                         _ext.stream()))
+        self.net.apply(self.n, self.rr, self.ld, self.rn, self.D, self.n3, self.zn, self.ld, sel=sel)
+        # z = z + zn, then maxit post sweeps from z
+        _ext.check(self.lib.mdp_axpby(m, sel.data_ptr(), 1.0, self.zn.data_ptr(), 1.0, cur.data_ptr(), self.ld,
+                                      self.n3, _ext.stream()))
+        src = cur
+        for it in range(maxit):
+            out = Z if it == maxit - 1 else (self.t2 if src is self.t1 else self.t1)
+            C.jacobi(V, src, out, omega, self.tmp, sel)
+            src = out
+        if maxit == 0 and cur is not Z:
+            Z.index_copy_(0, sel.long(), cur.index_select(0, sel.long()))
+
+
+def _single_problem(C):
+    if C is None:
+        return None
+    if not hasattr(C, "jacobi"):
+        raise TypeError("C must be this package's reduced_operator (device)")
+    return C
+
+
+def apply_neural(params, r, dfield: DistanceField, smoothing=None, C=None, zero_distance: bool = False,
+                 path: int = PATH_TCGEN05):
+    """One preconditioner application z ~ C^-1 r (training.py:290-319)."""
+    import torch
+    r = np.asarray(r, dtype=float)
+    if r.shape != (dfield.grid.num_nodes,):
+        raise ValueError("residual length must match the grid")
+    if smoothing is not None and C is None:
+        raise ValueError("smoothing needs the reduced operator")
+    C = _single_problem(C)
+    n = dfield.grid.n
+    n3 = n ** 3
+    ld = C.prob.ld if C is not None else n3
+    P = BatchedNeural(device_net(params, path), torch.as_tensor(dfield.values, device="cuda")[None], n, ld, 1,
+                      C=C, smoothing=smoothing, zero_distance=zero_distance)
+    V = torch.zeros((1, ld), dtype=torch.float64, device="cuda")
+    V[0, :n3] = torch.as_tensor(r, device="cuda")
+    Z = torch.zeros_like(V)
+    sel = torch.zeros(1, dtype=torch.int32, device="cuda")
+    P.apply_device(V, Z, sel, [0])
+    return Z[0, :n3].cpu().numpy()
+
+
+def apply_batched(params, residuals: list, dfields: list, path: int = PATH_TCGEN05) -> list:
+    """Batched network pass over (r, dfield) pairs of one size (training.py:322-338)."""
+    import torch
+    if len(residuals) != len(dfields):
+        raise ValueError("need one distance field per residual")
+    sizes = {d.grid.n for d in dfields}
+    if len(sizes) != 1:
+        raise ValueError("batched application needs a single spatial size")
+    n = sizes.pop()
+    n3 = n ** 3
+    b = len(residuals)
+    R = torch.as_tensor(np.stack([np.asarray(r, dtype=float) for r in residuals]), device="cuda")
+    D = torch.as_tensor(np.stack([d.values for d in dfields]), device="cuda")
+    P = BatchedNeural(device_net(params, path), D, n, n3, b)
+    Z = torch.zeros_like(R)
+    sel = torch.arange(b, dtype=torch.int32, device="cuda")
+    P.apply_device(R, Z, sel, list(range(b)))
+    Zh = Z.cpu().numpy()
+    return [Zh[i].copy() for i in range(b)]
+
+
+class NeuralPreconditioner(Preconditioner):
+    """Stateless apply wrapper binding weights to one graph (training.py:341-355)."""
+
+    def __init__(self, params, dfield: DistanceField, smoothing=None, C=None, zero_distance: bool = False,
+                 path: int = PATH_TCGEN05):
+        import torch
+        self.params = params
+        self.dfield = dfield
+        self.smoothing = smoothing
+        self.C = _single_problem(C)
+        self.zero_distance = zero_distance
+        n = dfield.grid.n
+        ld = self.C.prob.ld if self.C is not None else n ** 3
+        if smoothing is not None and self.C is None:
+            raise ValueError("smoothing needs the reduced operator")
+        self._dev = BatchedNeural(device_net(params, path), torch.as_tensor(dfield.values, device="cuda")[None],
+                                  n, ld, 1, C=self.C, smoothing=smoothing, zero_distance=zero_distance)
+
+    def apply_device(self, V, Z, sel, idx=None):
+        self._dev.apply_device(V, Z, sel, idx)
+
+    def apply(self, r):
+        return apply_neural(self.params, r, self.dfield, self.smoothing, self.C, self.zero_distance)

@@ -1,0 +1,102 @@
+"""C-ABI library: loads without a GPU, exports every symbol the header declares."""
+
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2505_08491_b200 import _ext
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def header_symbols():
+    text = (ROOT / "include" / "mdp_b200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mdp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert header_symbols() == sorted(_ext.EXPORTED)
+
+
+def test_library_exports_all_symbols():
+    lib = _ext.load_library()
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_ext.LIB_PATH)], capture_output=True, text=True).stdout
+    for name in header_symbols():
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_ext.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_host_ilu_matches_oracle_bitwise():
+    # host-side native ILU(0) factor (no GPU): bitwise against the oracle restatement
+    import scipy.sparse as sp
+    import oracle
+    from paper_2505_08491_b200.krylov import ilu0
+    from conftest import golden
+    g = golden("asm_cfg2_nc8")
+    A = sp.csr_matrix((g["A11_data"], g["A11_indices"], g["A11_indptr"]), shape=tuple(g["A11_shape"]))
+    f = ilu0(A)
+    assert np.array_equal(f.data, g["ilu_data"])
+    assert np.array_equal(f.data, oracle.ilu0(A).data)
+    # level schedule is a valid topological order of the sweeps
+    pos = np.empty(len(f.perm_f), dtype=int)
+    lev = np.empty(len(f.perm_f), dtype=int)
+    for L in range(f.nlev_f):
+        for r in f.perm_f[f.lev_f[L]:f.lev_f[L + 1]]:
+            lev[r] = L
+    for i in range(A.shape[0]):
+        for p in range(f.indptr[i], f.diag_pos[i]):
+            assert lev[f.indices[p]] < lev[i]
+
+
+def test_zero_pivot_names_row():
+    import scipy.sparse as sp
+    from paper_2505_08491_b200.krylov import ilu0
+    with pytest.raises(ValueError, match="row 1"):
+        ilu0(sp.csr_matrix(np.array([[1.0, 1.0], [1.0, 1.0]])))
+    A = sp.csr_matrix(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    A.eliminate_zeros()
+    with pytest.raises(ValueError, match="diagonal"):
+        ilu0(A)
+
+
+def test_checkpoint_roundtrip_and_init_match_reference(tmp_path):
+    import hashlib
+    from paper_2505_08491_b200 import neural
+    from conftest import golden
+    g = golden("apply_solve_n9")
+    path = tmp_path / "p.mdu3"
+    neural.save_checkpoint(neural.perturbed_params(0), path)
+    assert hashlib.sha256(path.read_bytes()).hexdigest() == str(g["ckpt_sha256"])
+    p = neural.load_checkpoint(path)
+    assert p.num_params() == 1092657
+    with pytest.raises(ValueError, match="magic"):
+        bad = tmp_path / "bad"
+        bad.write_bytes(b"XXXX" + path.read_bytes()[4:])
+        neural.load_checkpoint(bad)
+    with pytest.raises(ValueError, match="truncated"):
+        bad = tmp_path / "trunc"
+        bad.write_bytes(path.read_bytes()[:5000])
+        neural.load_checkpoint(bad)
+
+
+def test_weight_packing_layouts():
+    from paper_2505_08491_b200 import neural
+    rng = np.random.default_rng(0)
+    k = rng.standard_normal((64, 32, 3, 3, 3)).astype(np.float32)
+    p1 = neural.pack_conv(k, neural.PATH_CUDA_CORE).reshape(4, 32, 27, 16)
+    assert p1[1, 5, 13, 7] == k[16 + 7, 5].ravel()[13]
+    p0 = neural.pack_conv(k, neural.PATH_TCGEN05).reshape(1, 27, 8, 64, 4)
+    assert abs(p0[0, 13, 2, 40, 3] - k[40, 2 * 4 + 3].ravel()[13]) <= 2e-3 * abs(k[40, 11].ravel()[13])
+    t = rng.standard_normal((64, 32, 2, 2, 2)).astype(np.float32)
+    pt = neural.pack_tconv(t).reshape(2, 64, 8, 16)
+    assert pt[1, 10, 5, 3] == t[10, 16 + 3].ravel()[5]

@@ -1,0 +1,113 @@
+"""GPU coupled-solve parity against the reference's solve_coupled.
+
+Gate: FGMRES iteration counts within +-2 of the reference's, same
+converged flag, final true residual <= rtol (BASELINE north star).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from conftest import golden  # noqa: E402
+
+
+def _n9():
+    from paper_2505_08491_b200 import assembly as A, geometry as G
+    g = golden("asm_n9_family")
+    graph = G.Graph1D(g["graph_vertices"], g["graph_edges"], 1e-3, tuple(int(d) for d in g["dirichlet"]))
+    return A.assemble_coupled_system(G.StructuredGrid(9), graph, A.PhysicalParams())
+
+
+def _params(tmp_path, seed=0):
+    from paper_2505_08491_b200 import neural
+    path = tmp_path / "p.mdu3"
+    neural.save_checkpoint(neural.perturbed_params(seed), path)
+    return neural.load_checkpoint(path)
+
+
+@pytest.mark.parametrize("label", ["none", "neural_s"])
+def test_solve_coupled_n9_vs_reference(gpu, label, tmp_path):
+    from paper_2505_08491_b200 import harness
+    g = golden("apply_solve_n9")
+    s = _n9()
+    spec = {"type": "none"}
+    if label == "neural_s":
+        spec = {"type": "neural", "params": _params(tmp_path), "smoothing": {"maxit": 2}}
+    st = harness.CoupledStrategy(tol=1e-6, maxit=120, restart=30, inner_iterations=3, three_d=spec)
+    u3, u1, rep = harness.solve_coupled(s, st)
+    want = int(g[f"solve_{label}_iters"])
+    assert rep.converged == bool(g[f"solve_{label}_conv"])
+    if label == "none":
+        assert rep.iterations == want
+    else:
+        assert abs(rep.iterations - want) <= 2
+    assert rep.rel_residual <= 1e-6
+    assert all(u1[d] == 1.0 for d in s.dirichlet_nodes)
+    assert np.linalg.norm(u3 - g[f"solve_{label}_u3"]) <= 1e-4 * np.linalg.norm(g[f"solve_{label}_u3"])
+
+
+def _cfg1_system():
+    from paper_2505_08491_b200 import assembly as A, geometry as G
+    graph = G.Graph1D([[0.5, 0.5, 0.1], [0.5, 0.5, 0.9]], [[0, 1]], 0.02, (0,))
+    return A.assemble_coupled_system(G.StructuredGrid(17), graph, A.PhysicalParams(epsilon=0.02, beta=1.0),
+                                     n_circle=8, elems_per_edge=32)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("label", ["none", "neural_s"])
+def test_solve_cfg1_vs_reference(gpu, label, tmp_path):
+    from paper_2505_08491_b200 import harness
+    g = golden("solve_cfg1")
+    spec = {"type": "none"}
+    if label == "neural_s":
+        spec = {"type": "neural", "params": _params(tmp_path), "smoothing": {"maxit": 2}}
+    st = harness.CoupledStrategy(tol=1e-6, maxit=300, restart=30, inner_iterations=3, three_d=spec)
+    u3, u1, rep = harness.solve_coupled(_cfg1_system(), st)
+    want = int(g[f"{label}_iters"])
+    assert rep.converged == bool(g[f"{label}_conv"])
+    assert abs(rep.iterations - want) <= 2, (rep.iterations, want)
+    assert rep.rel_residual <= 1e-6
+    h = g[f"{label}_hist"]
+    k = min(10, len(h) - 1)
+    assert np.allclose(rep.residual_history[:k], h[:k], rtol=1e-3)
+
+
+def test_batched_solve_equals_serial(gpu, tmp_path):
+    from paper_2505_08491_b200 import assembly as A, geometry as G, harness
+    grid = G.StructuredGrid(17)
+    systems = [A.assemble_coupled_system(grid, G.random_tree(4, 30 + i, 0.02),
+                                         A.PhysicalParams(epsilon=0.02, beta=0.5 + 0.5 * i), elems_per_edge=8,
+                                         n_circle=8, bc3d="dirichlet", f1d=1.0) for i in range(3)]
+    spec = {"type": "neural", "params": _params(tmp_path, 2), "smoothing": {"maxit": 2}}
+    st = harness.CoupledStrategy(tol=1e-6, maxit=60, restart=30, inner_iterations=3, three_d=spec)
+    batched = harness.solve_coupled(systems, st)
+    for s, (u3b, u1b, rb) in zip(systems, batched):
+        u3, u1, r = harness.solve_coupled(s, st)
+        assert r.iterations == rb.iterations
+        assert r.converged == rb.converged
+        assert np.array_equal(u3, u3b) and np.array_equal(u1, u1b)
+
+
+def test_fgmres_dropin_with_device_operator(gpu, tmp_path):
+    from paper_2505_08491_b200 import assembly as A, geometry as G, krylov, training
+    import oracle
+    from oracle import problem as OP
+    s = _n9()
+    C = A.reduced_operator(s)
+    b = np.random.default_rng(5).standard_normal(s.n3)
+    x, rep = krylov.fgmres(C, None, b, restart=20, tol=1e-8, maxit=500)
+    g = golden("asm_n9_family")
+    o = OP.assemble_coupled_system(OP.StructuredGrid(9), OP.Graph(g["graph_vertices"], g["graph_edges"], 1e-3,
+                                                                  tuple(int(d) for d in g["dirichlet"])),
+                                   OP.PhysicalParams())
+    xo, ro = oracle.fgmres(OP.reduced_operator(o), None, b, restart=20, tol=1e-8, maxit=500)
+    assert abs(rep.iterations - ro.iterations) <= 2 and rep.converged
+    d = G.DistanceField(s.grid, np.zeros(s.n3))
+    P = training.NeuralPreconditioner(_params(tmp_path), d)
+    _, rep2 = krylov.fgmres(C, P, b, tol=1e-4, maxit=400)
+    assert rep2.iterations > 0 and len(rep2.residual_history) >= 2
+    with pytest.raises(TypeError):
+        krylov.fgmres(C, 3.0, b)
+    with pytest.raises(ValueError):
+        krylov.fgmres(C, None, b, restart=0)

@@ -1,0 +1,147 @@
+"""GPU parity of the CNN preconditioner (tcgen05 TF32 path and FP32 check path).
+
+Gate (BASELINE north star): relative L2 <= 2e-3 for the TF32 tensor-core
+apply against the reference's float64 network; the FP32 CUDA-core path is
+held to 1e-5.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from conftest import golden  # noqa: E402
+
+TF32_TOL = 2e-3
+FP32_TOL = 1e-5
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+def to_c4(x):
+    b, c, s = x.shape[:3]
+    return np.ascontiguousarray(x.reshape(b, c // 4, 4, s, s, s).transpose(0, 1, 3, 4, 5, 2), dtype=np.float32)
+
+
+def from_c4(y, c):
+    b, cq, s = y.shape[:3]
+    return y.transpose(0, 1, 5, 2, 3, 4).reshape(b, c, s, s, s)
+
+
+def run_layer(path, x, k, bias, relu=True, pool=False, out_extra_quads=0):
+    import torch
+    from paper_2505_08491_b200 import _ext, neural
+    lib = _ext.lib()
+    b, cin, S = x.shape[:3]
+    cout = k.shape[0]
+    So = S // 2 if pool else S
+    X = torch.as_tensor(to_c4(x), device="cuda")
+    W = torch.as_tensor(neural.pack_conv(k, path).ravel(), device="cuda")
+    Bt = torch.as_tensor(bias.astype(np.float32), device="cuda") if bias is not None else None
+    oq = cout // 4 + out_extra_quads
+    Y = torch.full((b, oq, So, So, So, 4), float("nan"), dtype=torch.float32, device="cuda")
+    _ext.check(lib.mdp_conv3_layer(path, b, S, cin, cout, X.data_ptr(), cin // 4, 0, W.data_ptr(),
+                                   None if Bt is None else Bt.data_ptr(), int(relu), Y.data_ptr(), oq,
+                                   out_extra_quads, int(pool), _ext.stream()))
+    y = Y.cpu().numpy()[:, out_extra_quads:]
+    return from_c4(y, cout), Y.cpu().numpy()
+
+
+SHAPES = [(16, 32), (32, 64), (64, 128), (128, 128), (128, 64), (64, 32)]
+
+
+@pytest.mark.parametrize("S", [8, 13, 17])
+@pytest.mark.parametrize("cin,cout", SHAPES)
+@pytest.mark.parametrize("path", [0, 1])
+def test_conv_layer_vs_oracle(gpu, S, cin, cout, path):
+    import oracle
+    rng = np.random.default_rng(S * 1000 + cin + cout)
+    x = rng.standard_normal((2, cin, S, S, S))
+    k = rng.standard_normal((cout, cin, 3, 3, 3)) * np.sqrt(2.0 / (27 * cin))
+    bias = rng.standard_normal(cout) * 0.1
+    ref = np.maximum(oracle.conv3d(x, k, bias), 0.0)
+    y, raw = run_layer(path, x, k, bias, out_extra_quads=2)
+    assert np.all(np.isnan(raw[:, :2])), "wrote outside its concat slot"
+    assert rel(y, ref) <= (TF32_TOL if path == 0 else FP32_TOL)
+
+
+@pytest.mark.parametrize("S", [8, 17, 33, 21])
+@pytest.mark.parametrize("cin,cout", [(32, 64), (64, 128)])
+def test_conv_pool_epilogue_vs_oracle(gpu, S, cin, cout):
+    import oracle
+    rng = np.random.default_rng(S + cin)
+    x = rng.standard_normal((1, cin, S, S, S))
+    k = rng.standard_normal((cout, cin, 3, 3, 3)) * np.sqrt(2.0 / (27 * cin))
+    ref = oracle.maxpool3d(np.maximum(oracle.conv3d(x, k, None), 0.0))
+    y, _ = run_layer(0, x, k, None, pool=True)
+    assert y.shape == ref.shape
+    assert rel(y, ref) <= TF32_TOL
+
+
+@pytest.mark.parametrize("path,tol", [(0, TF32_TOL), (1, FP32_TOL)])
+def test_unet_forward_vs_reference(gpu, path, tol):
+    from paper_2505_08491_b200 import neural
+    g = golden("unet_forward")
+    p = neural.perturbed_params(0)
+    for n in (9, 13, 17):
+        y = neural.unet_forward(p, g[f"x_n{n}"], path=path)
+        assert y.shape == (1, n, n, n)
+        assert rel(y, g[f"y_n{n}"]) <= tol, (n, rel(y, g[f"y_n{n}"]))
+    yb = neural.unet_forward(p, g["xb"], path=path)
+    assert rel(yb, g["yb"]) <= tol
+
+
+@pytest.mark.parametrize("n", [33, 65])
+def test_unet_forward_large_vs_oracle(gpu, n):
+    import oracle
+    from paper_2505_08491_b200 import neural
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((2, n, n, n))
+    x[0] /= np.linalg.norm(x[0])
+    x[1] = np.abs(x[1]) * 0.2
+    ref = oracle.unet_forward(oracle.noisy_params(1), x)
+    y = neural.unet_forward(neural.perturbed_params(1), x, path=0)
+    assert rel(y, ref) <= TF32_TOL
+
+
+def test_shipped_init_is_zero_map(gpu):
+    from paper_2505_08491_b200 import neural
+    x = np.random.default_rng(0).standard_normal((2, 9, 9, 9))
+    assert np.all(neural.unet_forward(neural.init_unet_params(3), x) == 0.0)
+
+
+def _n9():
+    from paper_2505_08491_b200 import assembly as A, geometry as G
+    g = golden("asm_n9_family")
+    graph = G.Graph1D(g["graph_vertices"], g["graph_edges"], 1e-3, tuple(int(d) for d in g["dirichlet"]))
+    return A.assemble_coupled_system(G.StructuredGrid(9), graph, A.PhysicalParams())
+
+
+def test_apply_neural_and_batched_vs_reference(gpu, tmp_path):
+    from paper_2505_08491_b200 import assembly as A, geometry as G, neural, training
+    g = golden("apply_solve_n9")
+    s = _n9()
+    path = tmp_path / "p.mdu3"
+    neural.save_checkpoint(neural.perturbed_params(0), path)
+    p = neural.load_checkpoint(path)
+    d = G.DistanceField(s.grid, g["dfield_mesh"])
+    z = training.apply_neural(p, g["r"], d)
+    assert rel(z, g["z_plain"]) <= TF32_TOL
+    C = A.reduced_operator(s)
+    zs = training.apply_neural(p, g["r"], d, smoothing=(2, 2.0 / 3.0), C=C)
+    assert rel(zs, g["z_smooth"]) <= TF32_TOL
+    zb = training.apply_batched(p, list(g["rs"]), [d] * 4)
+    for a, b in zip(zb[:3], g["zs_batched"][:3]):
+        assert rel(a, b) <= TF32_TOL
+    assert np.all(zb[3] == 0.0)
+    # batched == serial (bitwise on the device)
+    for r, zz in zip(g["rs"][:3], zb[:3]):
+        assert np.array_equal(training.apply_neural(p, r, d), zz)
+    # zero residual -> zero; exact homogeneity for a power of two
+    assert np.all(training.apply_neural(p, np.zeros(s.n3), d) == 0.0)
+    z4 = training.apply_neural(p, 4.0 * g["r"], d)
+    assert np.array_equal(z4, 4.0 * training.apply_neural(p, g["r"], d))
+    with pytest.raises(ValueError, match="operator"):
+        training.apply_neural(p, g["r"], d, smoothing=(2, 0.5))
