@@ -138,6 +138,7 @@ typedef struct mdp_ilu {
   const int32_t* perm_b;
   const int32_t* nlev_f;     /* [nsys]                                     */
   const int32_t* nlev_b;     /* [nsys]                                     */
+  int32_t max_rows, max_nnz; /* per-system maxima (shared-memory staging)  */
 } mdp_ilu;
 
 /* z1 = (LU)^-1 r1, bitwise equal to krylov.ilu0_apply (krylov.py:219-233,
@@ -186,6 +187,23 @@ int mdp_axpby(int32_t nsel, const int32_t* sel, double a, const double* x, doubl
 int mdp_copy_vec(int32_t nsel, const int32_t* sel, const double* src, int64_t lds,
                  double* dst, int64_t ldd, const int32_t* dst_slot, int64_t slot_stride,
                  int64_t n, void* stream);
+
+/* Device-side Hessenberg work of the fixed-step inner FGMRES
+ * (harness.py:385-387: restart = maxit = m, tol = 1e-300), the same
+ * arithmetic as krylov.py:142-172.  State per selection index i:
+ * H [(k+1) x k], cs, sn [k], g [k+1], flag (0 ok, 1 breakdown, 2 lucky
+ * breakdown, 4 zero rhs -- flagged systems are re-solved by the host path). */
+int mdp_fixed_init(int32_t nsel, int32_t k, const double* beta, double* H, double* cs, double* sn,
+                   double* g, double* flag, void* stream);
+int mdp_givens_step(int32_t nsel, int32_t k, int32_t j, const double* hcol, double* H, double* cs,
+                    double* sn, double* g, double* flag, void* stream);
+int mdp_backsub(int32_t nsel, int32_t k, int32_t m, const double* H, const double* g,
+                const double* flag, double* y, void* stream);
+/* dst_s <- src_s[slot[i]] (gather one vector out of a per-system slot array). */
+int mdp_copy_slot(int32_t nsel, const int32_t* sel, const double* src, int64_t lds, const int32_t* slot,
+                  int64_t slot_stride, double* dst, int64_t ldd, int64_t n, void* stream);
+/* y_s[0..n) = v */
+int mdp_fill(int32_t nsel, const int32_t* sel, double* y, int64_t ld, int64_t n, double v, void* stream);
 
 /* ------------------------------------------------------------------ */
 /* CNN preconditioner (neural.py:423-472, training.py:290-338).          */

@@ -34,7 +34,8 @@ class MdpProblem(C.Structure):
 class MdpIlu(C.Structure):
     _fields_ = [("nsys", _i32), ("lev_stride", _i32), ("row_start", _vp), ("ptr", _vp),
                 ("col", _vp), ("val", _vp), ("diag", _vp), ("lev_f", _vp), ("perm_f", _vp),
-                ("lev_b", _vp), ("perm_b", _vp), ("nlev_f", _vp), ("nlev_b", _vp)]
+                ("lev_b", _vp), ("perm_b", _vp), ("nlev_f", _vp), ("nlev_b", _vp),
+                ("max_rows", _i32), ("max_nnz", _i32)]
 
 
 class MdpUnet(C.Structure):
@@ -61,6 +62,11 @@ _SIGS = {
     "mdp_residual": (_i32, [_i32, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "mdp_axpby": (_i32, [_i32, _vp, _f64, _vp, _f64, _vp, _i64, _i64, _vp]),
     "mdp_copy_vec": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
+    "mdp_fixed_init": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mdp_givens_step": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mdp_backsub": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "mdp_fill": (_i32, [_i32, _vp, _vp, _i64, _i64, _f64, _vp]),
+    "mdp_copy_slot": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
     "mdp_unet_workspace_bytes": (C.c_size_t, [_i32, _i32, _i32]),
     "mdp_unet_apply": (_i32, [C.POINTER(MdpUnet), _i32, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _i64,
                               _vp, C.c_size_t, _vp]),

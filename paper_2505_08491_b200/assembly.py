@@ -384,9 +384,16 @@ class DeviceProblem:
             T.sort_indices()
             q0 = q_start[-1]
             Q = T.shape[0]
-            t_ptr.extend((T.indptr[1:] + t_ptr[-1]).tolist())
-            t_col.append(T.indices.astype(np.int32))
-            t_val.append(T.data)
+            Tg = T
+            if bmask is not None:
+                # eliminated cube nodes carry no value in the gather (M00 columns dropped)
+                keep = ~bmask[T.indices]
+                rows = np.repeat(np.arange(Q), np.diff(T.indptr))[keep]
+                Tg = sp.csr_matrix((T.data[keep], (rows, T.indices[keep])), shape=T.shape)
+                Tg.sort_indices()
+            t_ptr.extend((Tg.indptr[1:] + t_ptr[-1]).tolist())
+            t_col.append(Tg.indices.astype(np.int32))
+            t_val.append(Tg.data)
             psi = s.restriction.basis_1d.tocsr()
             psi.sort_indices()
             if np.any(np.diff(psi.indptr) != 2):

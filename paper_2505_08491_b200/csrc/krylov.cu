@@ -18,6 +18,55 @@ inline int red_blocks(int64_t n) {
   return nb < 1 ? 1 : (nb > cap ? cap : nb);
 }
 
+// Deterministic grid reduction without a second launch: every block
+// writes its partial row, the last block to finish (atomic ticket per
+// system) sums the partials in a fixed order (lane-strided, then a
+// shuffle tree) and resets the ticket.  The order depends on n and the SM
+// count only, never on the batch.
+struct RedOut {
+  double* out;      // [nsel][ostride]
+  int ostride;
+  int nk;           // entries to reduce
+  int mode;         // 0 plain, 1 sqrt, 2 arnoldi finalize (out = ||w||^2)
+  const double* h1; // mode 2: the two projections, [nsel][kmax+1]
+  const double* h2;
+  double* hcol;     // mode 2: [nsel][kmax+2] Hessenberg column + ||w||
+  int kmax;
+  const int32_t* nvs;
+};
+
+__device__ __forceinline__ void finish_reduction(const double* __restrict__ partial, int pstride,
+                                                 unsigned int* ticket, const RedOut& R, const double* mine) {
+  __shared__ bool last;
+  const int i = blockIdx.y;
+  if (threadIdx.x == 0) {
+    double* dst = const_cast<double*>(partial) + ((int64_t)i * gridDim.x + blockIdx.x) * pstride;
+    for (int k = 0; k < R.nk; ++k) dst[k] = mine[k];
+    __threadfence();
+    last = atomicAdd(&ticket[i], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* base = partial + (int64_t)i * gridDim.x * pstride;
+  for (int k = wid; k < R.nk; k += nw) {
+    double t = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) t += __ldcg(base + (int64_t)b * pstride + k);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) R.out[i * R.ostride + k] = R.mode == 1 ? sqrt(t) : t;
+  }
+  if (R.mode == 2) {  // hcol[k] = h1 + h2 (k < nv), hcol[kmax+1] = ||w||
+    __syncthreads();
+    const int nv = R.nvs[i];
+    for (int k = threadIdx.x; k <= R.kmax; k += blockDim.x)
+      R.hcol[i * (R.kmax + 2) + k] = k < nv ? R.h1[i * (R.kmax + 1) + k] + R.h2[i * (R.kmax + 1) + k] : 0.0;
+    if (threadIdx.x == 0) R.hcol[i * (R.kmax + 2) + R.kmax + 1] = sqrt(R.out[i * R.ostride]);
+  }
+  if (threadIdx.x == 0) ticket[i] = 0u;
+}
+
 // One pass over V[0..nv) and w for a block's chunk of elements.
 //   DOT:      acc_k = sum V_k w
 //   UPD_DOT:  w <- w - sum c_k V_k ; acc_k = sum V_k w
@@ -29,9 +78,11 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
                                                          const int32_t* __restrict__ nvs, double* w,
                                                          int64_t ldw, int64_t n,
                                                          const double* __restrict__ coef, int cstride,
-                                                         double* __restrict__ partial, int pstride) {
+                                                         double* __restrict__ partial, int pstride,
+                                                         unsigned int* ticket, RedOut R) {
   __shared__ double sh[32];
   __shared__ double csh[NV > 0 ? NV : 1];
+  __shared__ double mine[NV > 0 ? NV : 1];
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
   const int nv = nvs ? nvs[i] : 0;
@@ -63,36 +114,16 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
       acc[0] += we * we;
     }
   }
-  double* out = partial + ((int64_t)i * gridDim.x + blockIdx.x) * pstride;
+  const int nk = (NACC > 1) ? nv : 1;
 #pragma unroll
   for (int k = 0; k < NACC; ++k) {
-    if (NACC > 1 && k >= nv) break;
+    if (k >= nk) break;
     double t = block_sum(acc[k], sh);
-    if (threadIdx.x == 0) out[k] = t;
+    if (threadIdx.x == 0) mine[k] = t;
   }
-}
-
-// out[i][k] = sum_b partial[i][b][k] in block order; one CTA per system.
-__global__ void reduce_partials_kernel(const double* __restrict__ partial, int nblk, int pstride,
-                                       int nk, double* __restrict__ out, int ostride) {
-  const int i = blockIdx.x;
-  for (int k = threadIdx.x; k < nk; k += blockDim.x) {
-    double t = 0.0;
-    const double* p = partial + (int64_t)i * nblk * pstride + k;
-    for (int b = 0; b < nblk; ++b) t += p[(int64_t)b * pstride];
-    out[i * ostride + k] = t;
-  }
-}
-
-// hcol[i][k] = h1 + h2 (k < nv), hcol[i][kmax+1] = ||w||
-__global__ void arnoldi_finalize_kernel(const int32_t* __restrict__ nvs, const double* h1,
-                                        const double* h2, const double* nrm2, int kmax,
-                                        double* hcol) {
-  const int i = blockIdx.x;
-  const int nv = nvs[i];
-  for (int k = threadIdx.x; k <= kmax; k += blockDim.x)
-    hcol[i * (kmax + 2) + k] = k < nv ? h1[i * (kmax + 1) + k] + h2[i * (kmax + 1) + k] : 0.0;
-  if (threadIdx.x == 0) hcol[i * (kmax + 2) + kmax + 1] = sqrt(nrm2[i]);
+  RedOut Rl = R;
+  Rl.nk = nk;
+  finish_reduction(partial, pstride, ticket, Rl, mine);
 }
 
 // V[s][nv] = w / hn  (and vcur), exact division like krylov.py:165
@@ -118,10 +149,11 @@ __global__ void arnoldi_next_kernel(const int32_t* sel, double* V, int64_t ldv_s
 template <int MODE>
 static void launch_orth(int nv_max, dim3 grid, cudaStream_t st, const int32_t* sel, const double* V,
                         int64_t ldv_sys, int64_t ldv_vec, const int32_t* nvs, double* w, int64_t ldw,
-                        int64_t n, const double* coef, int cstride, double* partial, int pstride) {
+                        int64_t n, const double* coef, int cstride, double* partial, int pstride,
+                        unsigned int* ticket, const RedOut& R) {
 #define MDP_ORTH(NVT)                                                                            \
   orth_pass_kernel<NVT, MODE><<<grid, 128, 0, st>>>(sel, V, ldv_sys, ldv_vec, nvs, w, ldw, n, \
-                                                    coef, cstride, partial, pstride)
+                                                    coef, cstride, partial, pstride, ticket, R)
   if (MODE == NORM) {
     MDP_ORTH(0);
   } else if (nv_max <= 4) {
@@ -172,11 +204,13 @@ __global__ void basis_update_kernel(const int32_t* sel, double* x, int64_t ldx,
   }
 }
 
-// r = b - y, partial sum of squares
+// r = b - y and ||r|| (fused deterministic reduction)
 __global__ void __launch_bounds__(128) residual_kernel(const int32_t* sel, const double* __restrict__ b,
                                                         const double* __restrict__ y, double* r,
-                                                        int64_t ld, int64_t n, double* partial) {
+                                                        int64_t ld, int64_t n, double* partial,
+                                                        unsigned int* ticket, RedOut R) {
   __shared__ double sh[32];
+  __shared__ double mine[1];
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
   const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
@@ -188,12 +222,8 @@ __global__ void __launch_bounds__(128) residual_kernel(const int32_t* sel, const
     acc += v * v;
   }
   double t = block_sum(acc, sh);
-  if (threadIdx.x == 0) partial[(int64_t)i * gridDim.x + blockIdx.x] = t;
-}
-
-__global__ void sqrt_kernel(double* v, int m) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m) v[i] = sqrt(v[i]);
+  if (threadIdx.x == 0) mine[0] = t;
+  finish_reduction(partial, 1, ticket, R, mine);
 }
 
 __global__ void axpby_kernel(const int32_t* sel, double a, const double* __restrict__ x, double b,
@@ -221,41 +251,142 @@ __global__ void copy_vec_kernel(const int32_t* sel, const double* __restrict__ s
 // ILU(0) sweeps, one CTA per system, level-scheduled.  The per-row
 // arithmetic is the reference's sequential sum with explicitly rounded
 // operations (no FMA contraction), so results equal krylov.ilu0_apply
-// bitwise.
+// bitwise.  The system's factor is first staged in shared memory (when it
+// fits) so each level costs a barrier plus shared-memory latency only.
 __global__ void __launch_bounds__(256) ilu0_apply_kernel(const mdp_ilu F, const int32_t* sel,
                                                           const double* __restrict__ r,
-                                                          double* __restrict__ z, int64_t ld) {
+                                                          double* __restrict__ z, int64_t ld, int staged) {
   extern __shared__ double xsh[];
   const int s = sys_of(sel, blockIdx.x);
   const int rs = F.row_start[s], nrow = F.row_start[s + 1] - rs;
+  const int p0 = F.ptr[rs], nnz = F.ptr[rs + nrow] - p0;
+  double* vsh = xsh + nrow;
+  int* csh = (int*)(vsh + (staged ? nnz : 0));
+  int* psh = csh + (staged ? nnz : 0);
+  int* dsh = psh + (staged ? nrow + 1 : 0);
+  const double* val = F.val + p0;
+  const int* col = F.col + p0;
+  if (staged) {
+    for (int t = threadIdx.x; t < nnz; t += blockDim.x) {
+      vsh[t] = val[t];
+      csh[t] = col[t];
+    }
+    for (int t = threadIdx.x; t <= nrow; t += blockDim.x) psh[t] = F.ptr[rs + t] - p0;
+    for (int t = threadIdx.x; t < nrow; t += blockDim.x) dsh[t] = F.diag[rs + t] - p0;
+    val = vsh;
+    col = csh;
+  }
   const double* rp = r + s * ld;
   const int* levf = F.lev_f + (int64_t)s * F.lev_stride;  // nlev+1 boundaries
   const int* levb = F.lev_b + (int64_t)s * F.lev_stride;
   const int* pf = F.perm_f + rs;
   const int* pb = F.perm_b + rs;
+  __syncthreads();
   for (int L = 0; L < F.nlev_f[s]; ++L) {
     for (int t = levf[L] + threadIdx.x; t < levf[L + 1]; t += blockDim.x) {
-      int row = pf[t];
-      int g = rs + row;
+      const int row = pf[t];
+      const int a = staged ? psh[row] : F.ptr[rs + row] - p0;
+      const int d = staged ? dsh[row] : F.diag[rs + row] - p0;
       double acc = rp[row];
-      for (int p = F.ptr[g]; p < F.diag[g]; ++p) acc = __dsub_rn(acc, __dmul_rn(F.val[p], xsh[F.col[p]]));
+      for (int p = a; p < d; ++p) acc = __dsub_rn(acc, __dmul_rn(val[p], xsh[col[p]]));
       xsh[row] = acc;
     }
     __syncthreads();
   }
   for (int L = 0; L < F.nlev_b[s]; ++L) {
     for (int t = levb[L] + threadIdx.x; t < levb[L + 1]; t += blockDim.x) {
-      int row = pb[t];
-      int g = rs + row;
+      const int row = pb[t];
+      const int d = staged ? dsh[row] : F.diag[rs + row] - p0;
+      const int e = staged ? psh[row + 1] : F.ptr[rs + row + 1] - p0;
       double acc = xsh[row];
-      for (int p = F.diag[g] + 1; p < F.ptr[g + 1]; ++p)
-        acc = __dsub_rn(acc, __dmul_rn(F.val[p], xsh[F.col[p]]));
-      xsh[row] = __ddiv_rn(acc, F.val[F.diag[g]]);
+      for (int p = d + 1; p < e; ++p) acc = __dsub_rn(acc, __dmul_rn(val[p], xsh[col[p]]));
+      xsh[row] = __ddiv_rn(acc, val[d]);
     }
     __syncthreads();
   }
   double* zp = z + s * ld;
   for (int t = threadIdx.x; t < nrow; t += blockDim.x) zp[t] = xsh[t];
+}
+
+// ---- device-side Hessenberg work for the fixed-step inner FGMRES ----------
+// Same arithmetic as krylov.py:142-172 (explicitly rounded, no FMA); state
+// per selection index i: H [(k+1) x k] row-major, cs, sn [k], g [k+1].
+// flag: 0 ok, 1 Arnoldi breakdown, 2 lucky breakdown, 4 zero right-hand side
+// (any nonzero flag sends the system through the host-driven exact path).
+__global__ void fixed_init_kernel(int nsel, int k, const double* __restrict__ beta, double* H, double* cs,
+                                  double* sn, double* g, double* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nsel) return;
+  for (int t = 0; t < (k + 1) * k; ++t) H[(int64_t)i * (k + 1) * k + t] = 0.0;
+  for (int t = 0; t < k; ++t) cs[i * k + t] = sn[i * k + t] = 0.0;
+  for (int t = 0; t <= k; ++t) g[i * (k + 1) + t] = 0.0;
+  g[i * (k + 1)] = beta[i];
+  flag[i] = beta[i] == 0.0 ? 4.0 : 0.0;
+}
+
+__global__ void givens_step_kernel(int nsel, int k, int j, const double* __restrict__ hcol, double* H, double* cs,
+                                   double* sn, double* g, double* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nsel || flag[i] != 0.0) return;
+  double* Hi = H + (int64_t)i * (k + 1) * k;
+  double* c = cs + i * k;
+  double* s = sn + i * k;
+  double* gi = g + i * (k + 1);
+  const double* hc = hcol + (int64_t)i * (k + 2);
+  for (int r = 0; r <= j; ++r) Hi[r * k + j] = hc[r];
+  const double hn = hc[k + 1];
+  for (int r = 0; r < j; ++r) {
+    double a = Hi[r * k + j], b = Hi[(r + 1) * k + j];
+    double t = __dadd_rn(__dmul_rn(c[r], a), __dmul_rn(s[r], b));
+    Hi[(r + 1) * k + j] = __dadd_rn(__dmul_rn(-s[r], a), __dmul_rn(c[r], b));
+    Hi[r * k + j] = t;
+  }
+  const double denom = hypot(Hi[j * k + j], hn);
+  if (denom < 1e-14) {
+    flag[i] = 1.0;
+    return;
+  }
+  c[j] = __ddiv_rn(Hi[j * k + j], denom);
+  s[j] = __ddiv_rn(hn, denom);
+  Hi[j * k + j] = denom;
+  gi[j + 1] = __dmul_rn(-s[j], gi[j]);
+  gi[j] = __dmul_rn(c[j], gi[j]);
+  if (hn < 1e-14) flag[i] = 2.0;
+}
+
+// y = H[:m,:m]^-1 g[:m] by back substitution (krylov.py:168-171)
+__global__ void backsub_kernel(int nsel, int k, int m, const double* __restrict__ H, const double* __restrict__ g,
+                               const double* __restrict__ flag, double* y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nsel) return;
+  const double* Hi = H + (int64_t)i * (k + 1) * k;
+  double* yi = y + i * k;
+  if (flag[i] != 0.0) {
+    for (int r = 0; r < k; ++r) yi[r] = 0.0;
+    return;
+  }
+  for (int r = m - 1; r >= 0; --r) {
+    double acc = 0.0;
+    for (int c = r + 1; c < m; ++c) acc = __dadd_rn(acc, __dmul_rn(Hi[r * k + c], yi[c]));
+    yi[r] = __ddiv_rn(__dsub_rn(g[i * (k + 1) + r], acc), Hi[r * k + r]);
+  }
+}
+
+__global__ void copy_slot_kernel(const int32_t* sel, const double* __restrict__ src, int64_t lds,
+                                 const int32_t* __restrict__ slot, int64_t slot_stride, double* __restrict__ dst,
+                                 int64_t ldd, int64_t n) {
+  const int i = blockIdx.y;
+  const int s = sys_of(sel, i);
+  const double* a = src + s * lds + (int64_t)slot[i] * slot_stride;
+  double* d = dst + s * ldd;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    d[e] = a[e];
+}
+
+__global__ void fill_kernel(const int32_t* sel, double* y, int64_t ld, int64_t n, double v) {
+  const int s = sys_of(sel, blockIdx.y);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    y[s * ld + e] = v;
 }
 
 inline dim3 ew_grid(int64_t n, int nsel) {
@@ -269,11 +400,32 @@ inline dim3 ew_grid(int64_t n, int nsel) {
 
 using namespace mdp;
 
+// workspace: [tickets: nsel, padded][partials nsel x nb x 65][h1, h2: nsel x (kmax+1)][nrm2: nsel]
+// The tickets sit at a fixed offset for every entry point sharing a
+// workspace and must start at zero: callers allocate the workspace zeroed
+// once; every kernel resets its tickets when it finishes.
+struct Work {
+  double* partial;
+  double* h1;
+  double* h2;
+  double* nrm2;
+  unsigned int* ticket;
+};
+static Work carve(void* work, int32_t nsel, int32_t kmax, int64_t n) {
+  Work W;
+  const int nb = red_blocks(n);
+  W.ticket = (unsigned int*)work;
+  W.partial = (double*)((char*)work + ((size_t)nsel * sizeof(unsigned int) + 255) / 256 * 256);
+  W.h1 = W.partial + (size_t)nsel * nb * 65;
+  W.h2 = W.h1 + (size_t)nsel * (kmax + 1);
+  W.nrm2 = W.h2 + (size_t)nsel * (kmax + 1);
+  return W;
+}
+
 extern "C" size_t mdp_arnoldi_work_bytes(int32_t nsel, int32_t kmax, int64_t n) {
   int nb = red_blocks(n);
-  size_t partial = (size_t)nsel * nb * 65;
-  size_t small = (size_t)nsel * (2 * (kmax + 1) + 1);
-  return (partial + small) * sizeof(double) + 256;
+  size_t d = (size_t)nsel * nb * 65 + (size_t)nsel * (2 * (kmax + 1) + 1);
+  return d * sizeof(double) + ((size_t)nsel * sizeof(unsigned int) + 255) / 256 * 256 + 256;
 }
 
 extern "C" int mdp_arnoldi(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys,
@@ -286,28 +438,31 @@ extern "C" int mdp_arnoldi(int32_t nsel, const int32_t* sel, double* V, int64_t 
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = red_blocks(n);
   const int pstride = 65;
-  double* partial = (double*)work;
-  double* h1 = partial + (size_t)nsel * nb * pstride;
-  double* h2 = h1 + (size_t)nsel * (kmax + 1);
-  double* nrm2 = h2 + (size_t)nsel * (kmax + 1);
+  Work W = carve(work, nsel, kmax, n);
   dim3 grid(nb, nsel);
   const int nvmax = kmax + 1;
-  launch_orth<DOT>(nvmax, grid, st, sel, V, ldv_sys, ldv_vec, nv, w, ldw, n, nullptr, 0, partial, pstride);
+  RedOut R{};
+  R.out = W.h1;
+  R.ostride = kmax + 1;
+  R.mode = 0;
+  launch_orth<DOT>(nvmax, grid, st, sel, V, ldv_sys, ldv_vec, nv, w, ldw, n, nullptr, 0, W.partial, pstride,
+                   W.ticket, R);
   MDP_LAUNCH_CHECK("orth_pass DOT");
-  reduce_partials_kernel<<<nsel, 64, 0, st>>>(partial, nb, pstride, kmax + 1, h1, kmax + 1);
-  MDP_LAUNCH_CHECK("reduce_partials");
-  launch_orth<UPD_DOT>(nvmax, grid, st, sel, V, ldv_sys, ldv_vec, nv, w, ldw, n, h1, kmax + 1, partial,
-                       pstride);
+  R.out = W.h2;
+  launch_orth<UPD_DOT>(nvmax, grid, st, sel, V, ldv_sys, ldv_vec, nv, w, ldw, n, W.h1, kmax + 1, W.partial,
+                       pstride, W.ticket, R);
   MDP_LAUNCH_CHECK("orth_pass UPD_DOT");
-  reduce_partials_kernel<<<nsel, 64, 0, st>>>(partial, nb, pstride, kmax + 1, h2, kmax + 1);
-  MDP_LAUNCH_CHECK("reduce_partials");
-  launch_orth<UPD_NORM>(nvmax, grid, st, sel, V, ldv_sys, ldv_vec, nv, w, ldw, n, h2, kmax + 1, partial,
-                        pstride);
+  R.out = W.nrm2;
+  R.ostride = 1;
+  R.mode = 2;
+  R.h1 = W.h1;
+  R.h2 = W.h2;
+  R.hcol = hcol;
+  R.kmax = kmax;
+  R.nvs = nv;
+  launch_orth<UPD_NORM>(nvmax, grid, st, sel, V, ldv_sys, ldv_vec, nv, w, ldw, n, W.h2, kmax + 1, W.partial,
+                        pstride, W.ticket, R);
   MDP_LAUNCH_CHECK("orth_pass UPD_NORM");
-  reduce_partials_kernel<<<nsel, 32, 0, st>>>(partial, nb, pstride, 1, nrm2, 1);
-  MDP_LAUNCH_CHECK("reduce_partials");
-  arnoldi_finalize_kernel<<<nsel, 64, 0, st>>>(nv, h1, h2, nrm2, kmax, hcol);
-  MDP_LAUNCH_CHECK("arnoldi_finalize");
   arnoldi_next_kernel<<<ew_grid(n, nsel), 256, 0, st>>>(sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n,
                                                          hcol, vcur, ldc);
   MDP_LAUNCH_CHECK("mdp_arnoldi");
@@ -320,14 +475,13 @@ extern "C" int mdp_norms(int32_t nsel, const int32_t* sel, const double* x, int6
   MDP_REQUIRE(n > 0, "empty vectors");
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = red_blocks(n);
-  double* partial = (double*)work;
-  orth_pass_kernel<0, NORM><<<dim3(nb, nsel), 128, 0, st>>>(sel, nullptr, 0, 0, nullptr,
-                                                            const_cast<double*>(x), ldx, n, nullptr, 0,
-                                                            partial, 1);
-  MDP_LAUNCH_CHECK("orth_pass NORM");
-  reduce_partials_kernel<<<nsel, 32, 0, st>>>(partial, nb, 1, 1, out, 1);
-  MDP_LAUNCH_CHECK("reduce_partials");
-  sqrt_kernel<<<ceil_div(nsel, 128), 128, 0, st>>>(out, nsel);
+  Work W = carve(work, nsel, 1, n);
+  RedOut R{};
+  R.out = out;
+  R.ostride = 1;
+  R.mode = 1;
+  orth_pass_kernel<0, NORM><<<dim3(nb, nsel), 128, 0, st>>>(sel, nullptr, 0, 0, nullptr, const_cast<double*>(x),
+                                                            ldx, n, nullptr, 0, W.partial, 1, W.ticket, R);
   MDP_LAUNCH_CHECK("mdp_norms");
   return MDP_OK;
 }
@@ -357,12 +511,13 @@ extern "C" int mdp_residual(int32_t nsel, const int32_t* sel, const double* b, c
   if (nsel == 0) return MDP_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = red_blocks(n);
-  double* partial = (double*)work;
-  residual_kernel<<<dim3(nb, nsel), 128, 0, st>>>(sel, b, y, r, ld, n, partial);
-  MDP_LAUNCH_CHECK("residual_kernel");
-  reduce_partials_kernel<<<nsel, 32, 0, st>>>(partial, nb, 1, 1, rn, 1);
-  MDP_LAUNCH_CHECK("reduce_partials");
-  sqrt_kernel<<<ceil_div(nsel, 128), 128, 0, st>>>(rn, nsel);
+  Work W = carve(work, nsel, 1, n);
+  RedOut R{};
+  R.out = rn;
+  R.ostride = 1;
+  R.nk = 1;
+  R.mode = 1;
+  residual_kernel<<<dim3(nb, nsel), 128, 0, st>>>(sel, b, y, r, ld, n, W.partial, W.ticket, R);
   MDP_LAUNCH_CHECK("mdp_residual");
   return MDP_OK;
 }
@@ -385,18 +540,66 @@ extern "C" int mdp_copy_vec(int32_t nsel, const int32_t* sel, const double* src,
   return MDP_OK;
 }
 
+extern "C" int mdp_fixed_init(int32_t nsel, int32_t k, const double* beta, double* H, double* cs, double* sn,
+                              double* g, double* flag, void* stream) {
+  if (nsel == 0) return MDP_OK;
+  fixed_init_kernel<<<ceil_div(nsel, 64), 64, 0, (cudaStream_t)stream>>>(nsel, k, beta, H, cs, sn, g, flag);
+  MDP_LAUNCH_CHECK("fixed_init_kernel");
+  return MDP_OK;
+}
+
+extern "C" int mdp_givens_step(int32_t nsel, int32_t k, int32_t j, const double* hcol, double* H, double* cs,
+                               double* sn, double* g, double* flag, void* stream) {
+  MDP_REQUIRE(j >= 0 && j < k, "givens column %d outside [0, %d)", j, k);
+  if (nsel == 0) return MDP_OK;
+  givens_step_kernel<<<ceil_div(nsel, 64), 64, 0, (cudaStream_t)stream>>>(nsel, k, j, hcol, H, cs, sn, g, flag);
+  MDP_LAUNCH_CHECK("givens_step_kernel");
+  return MDP_OK;
+}
+
+extern "C" int mdp_backsub(int32_t nsel, int32_t k, int32_t m, const double* H, const double* g,
+                           const double* flag, double* y, void* stream) {
+  MDP_REQUIRE(m >= 0 && m <= k, "back substitution size %d outside [0, %d]", m, k);
+  if (nsel == 0) return MDP_OK;
+  backsub_kernel<<<ceil_div(nsel, 64), 64, 0, (cudaStream_t)stream>>>(nsel, k, m, H, g, flag, y);
+  MDP_LAUNCH_CHECK("backsub_kernel");
+  return MDP_OK;
+}
+
+extern "C" int mdp_copy_slot(int32_t nsel, const int32_t* sel, const double* src, int64_t lds,
+                             const int32_t* slot, int64_t slot_stride, double* dst, int64_t ldd, int64_t n,
+                             void* stream) {
+  if (nsel == 0) return MDP_OK;
+  copy_slot_kernel<<<ew_grid(n, nsel), 256, 0, (cudaStream_t)stream>>>(sel, src, lds, slot, slot_stride, dst, ldd,
+                                                                       n);
+  MDP_LAUNCH_CHECK("copy_slot_kernel");
+  return MDP_OK;
+}
+
+extern "C" int mdp_fill(int32_t nsel, const int32_t* sel, double* y, int64_t ld, int64_t n, double v,
+                        void* stream) {
+  if (nsel == 0) return MDP_OK;
+  fill_kernel<<<ew_grid(n, nsel), 256, 0, (cudaStream_t)stream>>>(sel, y, ld, n, v);
+  MDP_LAUNCH_CHECK("fill_kernel");
+  return MDP_OK;
+}
+
 extern "C" int mdp_ilu0_apply(const mdp_ilu* f, int32_t nsel, const int32_t* sel, const double* r,
                               double* z, int64_t ld, void* stream) {
   MDP_REQUIRE(f != nullptr, "null ILU descriptor");
   if (nsel == 0) return MDP_OK;
-  // shared memory holds one system's solution; 1D blocks here are <= ~8k rows
-  const int smem = 64 * 1024;
+  const size_t cap = 200 * 1024;
+  const size_t base = (size_t)f->max_rows * sizeof(double);
+  const size_t full = base + (size_t)f->max_nnz * (sizeof(double) + sizeof(int)) +
+                      (size_t)(2 * f->max_rows + 1) * sizeof(int);
+  const int staged = full <= cap;
+  MDP_REQUIRE(base <= cap, "1D block of %d rows too large for the single-CTA sweep", f->max_rows);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(ilu0_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(ilu0_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
     attr = true;
   }
-  ilu0_apply_kernel<<<nsel, 256, smem, (cudaStream_t)stream>>>(*f, sel, r, z, ld);
+  ilu0_apply_kernel<<<nsel, 256, staged ? full : base, (cudaStream_t)stream>>>(*f, sel, r, z, ld, staged);
   MDP_LAUNCH_CHECK("mdp_ilu0_apply");
   return MDP_OK;
 }

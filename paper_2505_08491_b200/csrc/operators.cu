@@ -113,61 +113,74 @@ __global__ void __launch_bounds__(TX* TY) stencil_kernel(const mdp_problem P, co
   }
 }
 
-// s_q = W_q ((T x3)_q - (Psi D x1)_q)
-__global__ void pi_gather_kernel(const mdp_problem P, const int32_t* sel,
-                                 const double* __restrict__ x3, const double* __restrict__ x1,
-                                 int64_t ld, double* __restrict__ s_out) {
+// s_q = W_q ((T x3)_q - (Psi D x1)_q): one warp per quadrature row, lanes
+// over the row's (point, corner) entries (8 for the centreline, up to 64
+// for the 8-point ring average), warp-shuffle reduction.  Entries on
+// eliminated (Dirichlet) cube nodes are dropped from T at build time.
+__global__ void __launch_bounds__(256) pi_gather_kernel(const mdp_problem P, const int32_t* sel,
+                                                         const double* __restrict__ x3,
+                                                         const double* __restrict__ x1, int64_t ld,
+                                                         double* __restrict__ s_out) {
   const int s = sys_of(sel, blockIdx.y);
-  const int q = P.q_start[s] + blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int q = P.q_start[s] + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= P.q_start[s + 1]) return;
-  const int n = P.n;
-  const bool dir = P.bc3d != 0;
   double acc = 0.0;
   if (x3) {
     const double* xp = x3 + (int64_t)s * ld;
-    for (int k = P.t_ptr[q]; k < P.t_ptr[q + 1]; ++k) {
-      int col = P.t_col[k];
-      if (dir) {
-        int i = col % n, j = (col / n) % n, kz = col / (n * n);
-        if (on_boundary(i, j, kz, n)) continue;
-      }
-      acc += P.t_val[k] * __ldg(xp + col);
-    }
+    for (int k = P.t_ptr[q] + lane; k < P.t_ptr[q + 1]; k += 32) acc += P.t_val[k] * __ldg(xp + P.t_col[k]);
   }
-  if (x1) {
-    const double* xp = x1 + (int64_t)s * ld;
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      int col = P.psi_col[2 * q + e];
-      if (col >= 0) acc -= P.psi_val[2 * q + e] * xp[col];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    if (x1) {
+      const double* xp = x1 + (int64_t)s * ld;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        int col = P.psi_col[2 * q + e];
+        if (col >= 0) acc -= P.psi_val[2 * q + e] * xp[col];
+      }
     }
+    s_out[q] = P.wq[q] * acc;
   }
-  s_out[q] = P.wq[q] * acc;
 }
 
-// y3[u] += alpha w_s (T^T s)[u], one thread per touched free node (no atomics)
-__global__ void pi_pull_kernel(const mdp_problem P, const int32_t* sel, const double* __restrict__ sv,
-                               double alpha, double* __restrict__ y3, int64_t ld) {
+// y3[u] += alpha w_s (T^T s)[u]: 8 lanes per touched free node, no atomics
+__global__ void __launch_bounds__(256) pi_pull_kernel(const mdp_problem P, const int32_t* sel,
+                                                       const double* __restrict__ sv, double alpha,
+                                                       double* __restrict__ y3, int64_t ld) {
   const int s = sys_of(sel, blockIdx.y);
-  const int u = P.u_start[s] + blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= P.u_start[s + 1]) return;
+  const int sub = threadIdx.x & 7;
+  const int u = P.u_start[s] + blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3);
+  const bool live = u < P.u_start[s + 1];
   double acc = 0.0;
-  for (int k = P.u_ptr[u]; k < P.u_ptr[u + 1]; ++k) acc += P.u_val[k] * sv[P.u_q[k]];
-  y3[(int64_t)s * ld + P.u_node[u]] += alpha * P.wc[s] * acc;
+  if (live)
+    for (int k = P.u_ptr[u] + sub; k < P.u_ptr[u + 1]; k += 8) acc += P.u_val[k] * sv[P.u_q[k]];
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (live && sub == 0) y3[(int64_t)s * ld + P.u_node[u]] += alpha * P.wc[s] * acc;
 }
 
-// y1 = K11 x1 - w D Psi^T s
-__global__ void oned_kernel(const mdp_problem P, const int32_t* sel, const double* __restrict__ x1,
-                            const double* __restrict__ sv, double* __restrict__ y1, int64_t ld) {
+// y1 = K11 x1 - w D Psi^T s: 4 lanes per 1D row
+__global__ void __launch_bounds__(256) oned_kernel(const mdp_problem P, const int32_t* sel,
+                                                    const double* __restrict__ x1, const double* __restrict__ sv,
+                                                    double* __restrict__ y1, int64_t ld) {
   const int s = sys_of(sel, blockIdx.y);
-  const int r = P.r1_start[s] + blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= P.r1_start[s + 1]) return;
+  const int sub = threadIdx.x & 3;
+  const int r = P.r1_start[s] + blockIdx.x * (blockDim.x >> 2) + (threadIdx.x >> 2);
+  const bool live = r < P.r1_start[s + 1];
   const double* xp = x1 + (int64_t)s * ld;
-  double a = 0.0;
-  for (int k = P.k_ptr[r]; k < P.k_ptr[r + 1]; ++k) a += P.k_val[k] * xp[P.k_col[k]];
-  double b = 0.0;
-  for (int k = P.p_ptr[r]; k < P.p_ptr[r + 1]; ++k) b += P.p_val[k] * sv[P.p_q[k]];
-  y1[(int64_t)s * ld + (r - P.r1_start[s])] = a - P.wc[s] * b;
+  double a = 0.0, b = 0.0;
+  if (live) {
+    for (int k = P.k_ptr[r] + sub; k < P.k_ptr[r + 1]; k += 4) a += P.k_val[k] * xp[P.k_col[k]];
+    for (int k = P.p_ptr[r] + sub; k < P.p_ptr[r + 1]; k += 4) b += P.p_val[k] * sv[P.p_q[k]];
+  }
+#pragma unroll
+  for (int o = 2; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (live && sub == 0) y1[(int64_t)s * ld + (r - P.r1_start[s])] = a - P.wc[s] * b;
 }
 
 // x_out = x + (omega (r - Cx)) / diag  (Cx in tmp); x == NULL means x = 0 and Cx = 0
@@ -239,8 +252,8 @@ static int launch_stencil(const mdp_problem* p, int32_t nsel, const int32_t* sel
 static int launch_gather(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* x3,
                          const double* x1, int64_t ld, double* s, cudaStream_t st) {
   if (p->qmax <= 0) return MDP_OK;
-  dim3 grid(ceil_div(p->qmax, 128), nsel);
-  pi_gather_kernel<<<grid, 128, 0, st>>>(*p, sel, x3, x1, ld, s);
+  dim3 grid(ceil_div(p->qmax, 8), nsel);
+  pi_gather_kernel<<<grid, 256, 0, st>>>(*p, sel, x3, x1, ld, s);
   MDP_LAUNCH_CHECK("pi_gather_kernel");
   return MDP_OK;
 }
@@ -248,8 +261,8 @@ static int launch_gather(const mdp_problem* p, int32_t nsel, const int32_t* sel,
 static int launch_pull(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* s,
                        double alpha, double* y3, int64_t ld, cudaStream_t st) {
   if (p->umax <= 0) return MDP_OK;
-  dim3 grid(ceil_div(p->umax, 128), nsel);
-  pi_pull_kernel<<<grid, 128, 0, st>>>(*p, sel, s, alpha, y3, ld);
+  dim3 grid(ceil_div(p->umax, 32), nsel);
+  pi_pull_kernel<<<grid, 256, 0, st>>>(*p, sel, s, alpha, y3, ld);
   MDP_LAUNCH_CHECK("pi_pull_kernel");
   return MDP_OK;
 }
@@ -257,8 +270,8 @@ static int launch_pull(const mdp_problem* p, int32_t nsel, const int32_t* sel, c
 static int launch_oned(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* x1,
                        const double* s, double* y1, int64_t ld, cudaStream_t st) {
   if (p->r1max <= 0) return MDP_OK;
-  dim3 grid(ceil_div(p->r1max, 128), nsel);
-  oned_kernel<<<grid, 128, 0, st>>>(*p, sel, x1, s, y1, ld);
+  dim3 grid(ceil_div(p->r1max, 64), nsel);
+  oned_kernel<<<grid, 256, 0, st>>>(*p, sel, x1, s, y1, ld);
   MDP_LAUNCH_CHECK("oned_kernel");
   return MDP_OK;
 }

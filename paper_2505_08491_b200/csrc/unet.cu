@@ -160,8 +160,8 @@ __global__ void __launch_bounds__(128) tconv_kernel(const float4* __restrict__ i
   __syncthreads();
   const int So = 2 * Sin + op;
   const int64_t nvo = (int64_t)So * So * So, nvi = (int64_t)Sin * Sin * Sin;
-  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (v >= nvo) return;
+  // persistent over output voxels: the weights are staged once per block
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvo; v += (int64_t)gridDim.x * blockDim.x) {
   const int X = v % So, Y = (v / So) % So, Z = v / ((int64_t)So * So);
   float acc[16];
 #pragma unroll
@@ -183,6 +183,7 @@ __global__ void __launch_bounds__(128) tconv_kernel(const float4* __restrict__ i
                            fmaxf(acc[4 * q + 3], 0.f));
     if (round_tf32) o = tf32_round4(o);
     out[((int64_t)b * out_cq + out_q0 + g * 4 + q) * nvo + v] = o;
+  }
   }
 }
 
@@ -262,7 +263,10 @@ static int launch_tconv(int nb, const float4* in, int in_cq, int cin, int cout, 
     cudaFuncSetAttribute(tconv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 8 * 16 * 4);
     attr = true;
   }
-  dim3 grid(ceil_div((int64_t)So * So * So, 128), cout / 16, nb);
+  int bx = ceil_div((int64_t)So * So * So, 128);
+  const int cap = (2 * sm_count() + (cout / 16) * nb - 1) / ((cout / 16) * nb);
+  bx = bx > cap ? cap : bx;
+  dim3 grid(bx < 1 ? 1 : bx, cout / 16, nb);
   tconv_kernel<<<grid, 128, smem, st>>>(in, in_cq, cin, Sin, op, w, bias, out, out_cq, out_q0, round_tf32);
   MDP_LAUNCH_CHECK("tconv_kernel");
   return MDP_OK;

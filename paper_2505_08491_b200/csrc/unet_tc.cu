@@ -6,8 +6,9 @@
 // each z-plane is one M = 128 MMA row block, N = Cout, K = 27 taps x Cin.
 //
 // A operand: the brick plus its 1-voxel halo, (ZP+2) x 18 x 10 voxels x 32
-// channels, is fetched ONCE per 32-channel chunk by a single 5-D TMA box
-// from the channel-quad-blocked activation tensor, with TMA's out-of-bounds
+// channels, is fetched ONCE per 32-channel chunk by a single 4-D TMA box
+// (inner row = a 10-voxel x-run of one channel quad, 160 B) from the
+// channel-quad-blocked activation tensor, with TMA's out-of-bounds
 // zero fill providing the same-padding.  The box lands in shared memory as
 // [quad][z][y][x][4 floats], which is exactly the K-major no-swizzle UMMA
 // canonical layout (core matrix = 8 consecutive x-voxels x 16 B): every
@@ -19,11 +20,12 @@
 // B operand: weights pre-packed per (chunk, tap) as [quad][Cout][4 floats]
 // (K-major no-swizzle) and streamed with 1-D bulk copies.
 //
-// Warp roles (256 threads): w0 TMA/bulk producer, w1 MMA issuer, w2 TMEM
-// allocator, w4..w7 epilogue (TMEM -> registers -> bias/ReLU/TF32 round ->
+// Warp roles (256 threads): w0 weight (bulk) producer, w3 halo (TMA)
+// producer, w1 MMA issuer, w2 TMEM allocator, w4..w7 epilogue (TMEM -> registers -> bias/ReLU/TF32 round ->
 // global, optional fused 2x2x2 max-pool).  Two TMEM accumulator buffers let
 // the epilogue of tile t overlap the MMAs of tile t+1.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "unet_layout.cuh"
 
@@ -37,6 +39,7 @@ constexpr int QUAD_BYTES = HROWS * 16;
 
 struct ConvArgs {
   int nb, S, cin, cout, cqc, nchunk;
+  int nsplit, ncol;  // output channels split over nsplit CTAs of ncol each (small layers)
   int tx, ty, tz, ntiles;
   int in_cq, in_q0;
   const float* w;
@@ -46,6 +49,9 @@ struct ConvArgs {
   int out_cq, out_q0, Sout;
   uint32_t a_bytes, b_bytes;
   int na, nbs;
+  int resident;  // 1: the whole filter (27 taps, one chunk) stays in shared memory
+  int tps;       // taps per weight stage (one mbarrier handshake per stage)
+  int dbg;       // MDP_DEBUG_CONV bits (timing experiments only): 1 no stores, 2 no MMA, 4 no TMA, 8 no weight copies
   uint32_t tmem_cols;
   HeadArgs head;
 };
@@ -78,12 +84,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                            int c2, int c3, int c4) {
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3) {
   asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
 
@@ -113,6 +119,36 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// Start-address offset (16-byte units) of tap t's shifted view of the halo brick.
+__host__ __device__ constexpr uint32_t tap_off16(int t) {
+  return (uint32_t)(((t / 9) * HY + (t / 3) % 3) * HX + t % 3);
+}
+
+// Issue one weight stage: TPS taps x 2 K-steps (16-channel chunk = 2 x K8) x ZP
+// z-planes, fully unrolled.  Descriptors are built once per stage; every MMA
+// only adds compile-time constants to the 14-bit start-address fields
+// (addresses < 256 KB, no carry), so the single issuing thread spends a few
+// instructions per MMA instead of rebuilding 64-bit descriptors.
+template <int TPS>
+__device__ __forceinline__ void issue_stage(uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi,
+                                            uint32_t b_tap16, uint32_t b_ks16, uint32_t dcol, uint32_t ncol,
+                                            uint32_t idesc, uint32_t& accf) {
+#pragma unroll
+  for (int tt = 0; tt < TPS; ++tt) {
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo + tt * b_tap16 + ks * b_ks16);
+#pragma unroll
+      for (int zp = 0; zp < ZP; ++zp) {
+        const uint32_t off = tap_off16(tt) + (uint32_t)(zp * HY * HX) + (uint32_t)(ks * 2 * (QUAD_BYTES / 16));
+        const uint64_t ad = ((uint64_t)a_hi << 32) | (a_lo + off);
+        mma_tf32(dcol + zp * ncol, ad, bd, idesc, accf);
+        accf = 1u;
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -136,7 +172,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ void decode_tile(const ConvArgs& A, int tile, int& b, int& x0, int& y0, int& z0) {
+__device__ __forceinline__ void decode_tile(const ConvArgs& A, int tile, int& b, int& x0, int& y0, int& z0,
+                                            int& n0) {
+  n0 = (tile % A.nsplit) * A.ncol;
+  tile /= A.nsplit;
   int ix = tile % A.tx;
   int t = tile / A.tx;
   int iy = t % A.ty;
@@ -191,23 +230,58 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
   const uint32_t tmem = *tmem_slot;
   const int ntaps = 27;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- producer
-      int as = 0, ap = 0, bs = 0, bp = 0;
+  if (warp == 3) {
+    if (lane == 0) {  // ---------------- A producer: halo bricks, one TMA box per 32-channel chunk
+      int as = 0, ap = 0;
       for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
-        int b, x0, y0, z0;
-        decode_tile(A, tile, b, x0, y0, z0);
+        int b, x0, y0, z0, n0;
+        decode_tile(A, tile, b, x0, y0, z0, n0);
         for (int c = 0; c < A.nchunk; ++c) {
           mbar_wait(&a_empty[as], ap ^ 1);
-          mbar_expect_tx(&a_full[as], A.a_bytes);
-          tma_load_5d(sA + (size_t)as * A.a_bytes, &tmap, &a_full[as], 0, x0 - 1, y0 - 1, z0 - 1,
-                      b * A.in_cq + A.in_q0 + c * A.cqc);
+          if (A.dbg & 4) {
+            mbar_arrive(&a_full[as]);
+          } else {
+            mbar_expect_tx(&a_full[as], A.a_bytes);
+            // inner box row = 10 voxels x 4 channels (160 B); coordinate -4 floats = voxel x0-1
+            tma_load_4d(sA + (size_t)as * A.a_bytes, &tmap, &a_full[as], 4 * (x0 - 1), y0 - 1, z0 - 1,
+                        b * A.in_cq + A.in_q0 + c * A.cqc);
+          }
           if (++as == A.na) { as = 0; ap ^= 1; }
-          const float* wc = A.w + (size_t)c * ntaps * (A.b_bytes / 4);
-          for (int t = 0; t < ntaps; ++t) {
+        }
+      }
+    }
+  } else if (warp == 0) {
+    if (lane == 0) {  // ---------------- B producer: weight tiles per (chunk, tap)
+      int bs = 0, bp = 0;
+      for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
+        if (A.resident && tile != (int)blockIdx.x) break;  // resident filter: loaded once
+        int b, x0, y0, z0, n0;
+        decode_tile(A, tile, b, x0, y0, z0, n0);
+        for (int c = 0; c < A.nchunk; ++c) {
+          // packed weights [chunk][tap][quad][cout][4]; a stage holds tps
+          // consecutive taps: one contiguous copy when the CTA owns every
+          // output channel, else one per (tap, quad)
+          const size_t tap_floats = (size_t)A.cqc * A.cout * 4;
+          const float* wc = A.w + (size_t)c * ntaps * tap_floats;
+          for (int t0 = 0; t0 < ntaps; t0 += A.tps) {
             mbar_wait(&b_empty[bs], bp ^ 1);
+            if (A.dbg & 8) {
+              mbar_arrive(&b_full[bs]);
+              if (++bs == A.nbs) { bs = 0; bp ^= 1; }
+              continue;
+            }
             mbar_expect_tx(&b_full[bs], A.b_bytes);
-            bulk_load(sB + (size_t)bs * A.b_bytes, wc + (size_t)t * (A.b_bytes / 4), A.b_bytes, &b_full[bs]);
+            uint8_t* dst = sB + (size_t)bs * A.b_bytes;
+            const float* src = wc + (size_t)t0 * tap_floats;
+            if (A.nsplit == 1) {
+              bulk_load(dst, src, A.b_bytes, &b_full[bs]);
+            } else {
+              for (int tt = 0; tt < A.tps; ++tt)
+                for (int qd = 0; qd < A.cqc; ++qd)
+                  bulk_load(dst + ((size_t)tt * A.cqc + qd) * A.ncol * 16,
+                            src + (size_t)tt * tap_floats + ((size_t)qd * A.cout + n0) * 4, A.ncol * 16,
+                            &b_full[bs]);
+            }
             if (++bs == A.nbs) { bs = 0; bp ^= 1; }
           }
         }
@@ -215,36 +289,42 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(A.cout >> 3) << 17) |
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(A.ncol >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
       const uint32_t lbo_a = QUAD_BYTES, sbo_a = HX * 16;
-      const uint32_t lbo_b = A.cout * 16, sbo_b = 128;
+      const uint32_t lbo_b = A.ncol * 16, sbo_b = 128;
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
       int as = 0, ap = 0, bs = 0, bp = 0, li = 0;
       for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++li) {
         const int buf = li & 1;
         mbar_wait(&t_empty[buf], ((li >> 1) & 1) ^ 1);
         fence_after();
-        const uint32_t dcol = tmem + (uint32_t)(buf * ZP * A.cout);
+        const uint32_t dcol = tmem + (uint32_t)(buf * ZP * A.ncol);
+        uint32_t accf = 0u;  // the tile's first MMA overwrites the accumulator
         for (int c = 0; c < A.nchunk; ++c) {
           mbar_wait(&a_full[as], ap);
           fence_after();
           const uint32_t abase = a0 + as * A.a_bytes;
-          for (int t = 0; t < ntaps; ++t) {
-            mbar_wait(&b_full[bs], bp);
-            fence_after();
-            const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
-            const uint32_t bbase = b0 + bs * A.b_bytes;
-            for (int ks = 0; ks < A.cqc / 2; ++ks) {
-              const uint64_t bd = umma_desc(bbase + 2 * ks * lbo_b, lbo_b, sbo_b);
-#pragma unroll
-              for (int zp = 0; zp < ZP; ++zp) {
-                const uint32_t off = (uint32_t)(((zp + dz) * HY + dy) * HX + dx) * 16u;
-                const uint64_t ad = umma_desc(abase + 2 * ks * lbo_a + off, lbo_a, sbo_a);
-                mma_tf32(dcol + zp * A.cout, ad, bd, idesc, (c | t | ks) != 0);
+          for (int t0 = 0; t0 < ntaps; t0 += A.tps) {
+            if (!A.resident || li == 0) {
+              mbar_wait(&b_full[bs], bp);
+              fence_after();
+            }
+            const uint64_t ad0 = umma_desc(abase + tap_off16(t0) * 16u, lbo_a, sbo_a);
+            const uint64_t bd0 = umma_desc(b0 + bs * A.b_bytes, lbo_b, sbo_b);
+            const uint32_t a_lo = (uint32_t)ad0, a_hi = (uint32_t)(ad0 >> 32);
+            const uint32_t b_lo = (uint32_t)bd0, b_hi = (uint32_t)(bd0 >> 32);
+            const uint32_t b_tap16 = (uint32_t)(A.cqc * A.ncol);  // (cqc * ncol * 16 B) / 16
+            const uint32_t b_ks16 = (uint32_t)(2 * A.ncol);         // (2 * lbo_b) / 16
+            if (!(A.dbg & 2)) {
+              switch (A.tps) {
+                case 27: issue_stage<27>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
+                case 9: issue_stage<9>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
+                case 3: issue_stage<3>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
+                default: issue_stage<1>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
               }
             }
-            mma_commit(&b_empty[bs]);
+            if (!A.resident) mma_commit(&b_empty[bs]);
             if (++bs == A.nbs) { bs = 0; bp ^= 1; }
           }
           mma_commit(&a_empty[as]);
@@ -265,33 +345,34 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
     int li = 0;
     for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++li) {
       const int buf = li & 1;
-      int b, x0, y0, z0;
-      decode_tile(A, tile, b, x0, y0, z0);
+      int b, x0, y0, z0, n0;
+      decode_tile(A, tile, b, x0, y0, z0, n0);
       mbar_wait(&t_full[buf], (li >> 1) & 1);
       fence_after();
-      const uint32_t dcol = tmem + lane_addr + (uint32_t)(buf * ZP * A.cout);
+      const uint32_t dcol = tmem + lane_addr + (uint32_t)(buf * ZP * A.ncol);
+      const int q0 = A.out_q0 + n0 / 4;
       const int gx = x0 + lx, gy = y0 + ly;
       if (A.epi == EPI_POOL) {
         const int px = gx >> 1, py = gy >> 1, pz = z0 >> 1;
         const bool writer = ((lane & 1) == 0) && ((ly & 1) == 0) && px < So && py < So && pz < So;
-        for (int cg = 0; cg < A.cout / 16; ++cg) {
+        for (int cg = 0; cg < A.ncol / 16; ++cg) {
           float v0[16], v1[16];
           tmem_ld16(dcol + cg * 16, v0);
-          tmem_ld16(dcol + A.cout + cg * 16, v1);
+          tmem_ld16(dcol + A.ncol + cg * 16, v1);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float m = fmaxf(v0[i], v1[i]);
             m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
             m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
-            if (A.bias) m += A.bias[cg * 16 + i];
+            if (A.bias) m += A.bias[n0 + cg * 16 + i];
             if (A.relu) m = fmaxf(m, 0.f);
             v0[i] = tf32_round(m);
           }
-          if (writer) {
+          if (writer && !(A.dbg & 1)) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               float4 o = make_float4(v0[4 * q], v0[4 * q + 1], v0[4 * q + 2], v0[4 * q + 3]);
-              A.out[((int64_t)b * A.out_cq + A.out_q0 + cg * 4 + q) * So3 + ((int64_t)pz * So + py) * So + px] = o;
+              A.out[((int64_t)b * A.out_cq + q0 + cg * 4 + q) * So3 + ((int64_t)pz * So + py) * So + px] = o;
             }
           }
         }
@@ -300,21 +381,21 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
         for (int zp = 0; zp < ZP; ++zp) {
           const int gz = z0 + zp;
           const bool ok = gx < S && gy < S && gz < S;
-          for (int cg = 0; cg < A.cout / 16; ++cg) {
+          for (int cg = 0; cg < A.ncol / 16; ++cg) {
             float v[16];
-            tmem_ld16(dcol + zp * A.cout + cg * 16, v);
+            tmem_ld16(dcol + zp * A.ncol + cg * 16, v);
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               float m = v[i];
-              if (A.bias) m += A.bias[cg * 16 + i];
+              if (A.bias) m += A.bias[n0 + cg * 16 + i];
               if (A.relu) m = fmaxf(m, 0.f);
               v[i] = tf32_round(m);
             }
-            if (ok) {
+            if (ok && !(A.dbg & 1)) {
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                A.out[((int64_t)b * A.out_cq + A.out_q0 + cg * 4 + q) * S3 + ((int64_t)gz * S + gy) * S + gx] = o;
+                A.out[((int64_t)b * A.out_cq + q0 + cg * 4 + q) * S3 + ((int64_t)gz * S + gy) * S + gx] = o;
               }
             }
           }
@@ -366,12 +447,18 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   A.S = S;
   A.cin = cin;
   A.cout = cout;
-  A.cqc = cin >= 32 ? 8 : cin / 4;
+  A.cqc = 4;  // 16-channel chunks: a 46 KB halo per stage leaves room for deep multi-tap weight stages
   A.nchunk = cin / (4 * A.cqc);
   A.tx = ceil_div(S, BX);
   A.ty = ceil_div(S, BY);
   A.tz = ceil_div(S, ZP);
-  A.ntiles = nb * A.tx * A.ty * A.tz;
+  const int spatial = nb * A.tx * A.ty * A.tz;
+  // small layers (few bricks): split the output channels over CTAs, down to
+  // 32 per CTA, until the grid covers the SMs
+  A.nsplit = 1;
+  while (spatial * A.nsplit < sm_count() && cout / (2 * A.nsplit) >= 32) A.nsplit *= 2;
+  A.ncol = cout / A.nsplit;
+  A.ntiles = spatial * A.nsplit;
   A.in_cq = in_cq;
   A.in_q0 = in_q0;
   A.w = w;
@@ -383,29 +470,54 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   A.out_q0 = out_q0;
   A.Sout = epi == EPI_POOL ? S / 2 : S;
   A.a_bytes = (uint32_t)A.cqc * QUAD_BYTES;
-  A.b_bytes = (uint32_t)A.cqc * cout * 16;
   A.na = 2;
-  const size_t budget = 227 * 1024 - 2048;
-  int nbs = 6;
-  while (nbs > 2 && (size_t)A.na * A.a_bytes + (size_t)nbs * A.b_bytes > budget) --nbs;
+  const size_t budget = 227 * 1024 - 2048 - 1024;
+  const size_t tap_bytes = (size_t)A.cqc * A.ncol * 16;
+  A.resident = 0;
+  int nbs = 0;
+  if (A.nchunk == 1 && (size_t)A.na * A.a_bytes + 27 * tap_bytes <= budget) {
+    A.resident = 1;  // e.g. enc1b: the 27-tap filter fits next to the halo double buffer
+    A.tps = 27;
+    nbs = 1;
+  } else {
+    // as many taps per stage as leave >= 3 stages: each barrier handshake must
+    // cover enough MMA work to hide its ~500-cycle round trip
+    const int opts[3] = {9, 3, 1};
+    for (int o = 0; o < 3 && nbs == 0; ++o) {
+      A.tps = opts[o];
+      int k = (int)((budget - (size_t)A.na * A.a_bytes) / (tap_bytes * A.tps));
+      if (k >= 3 || (o == 2 && k >= 2)) nbs = k > 8 ? 8 : k;
+    }
+  }
+  A.b_bytes = (uint32_t)(tap_bytes * A.tps);
   A.nbs = nbs;
   MDP_REQUIRE((size_t)A.na * A.a_bytes + (size_t)nbs * A.b_bytes <= budget, "tc conv tile does not fit smem");
   uint32_t cols = 32;
-  while (cols < (uint32_t)(2 * ZP * cout)) cols <<= 1;
+  while (cols < (uint32_t)(2 * ZP * A.ncol)) cols <<= 1;
   A.tmem_cols = cols;
   if (head) A.head = *head;
+  {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("MDP_DEBUG_CONV");
+      dbg = e ? atoi(e) : 0;
+    }
+    A.dbg = dbg;
+  }
 
+  // 4-D view of the quad-blocked activations: (x * 4 + channel, y, z, item * CQ + quad);
+  // the innermost box row is a whole 10-voxel x-run (160 B) of one quad
   CUtensorMap map;
-  cuuint64_t gdim[5] = {4, (cuuint64_t)S, (cuuint64_t)S, (cuuint64_t)S, (cuuint64_t)nb * in_cq};
-  cuuint64_t gstride[4] = {16, (cuuint64_t)16 * S, (cuuint64_t)16 * S * S, (cuuint64_t)16 * S * S * S};
-  cuuint32_t box[5] = {4, HX, HY, HZ, (cuuint32_t)A.cqc};
-  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, (void*)in, gdim, gstride, box, estr,
+  cuuint64_t gdim[4] = {(cuuint64_t)4 * S, (cuuint64_t)S, (cuuint64_t)S, (cuuint64_t)nb * in_cq};
+  cuuint64_t gstride[3] = {(cuuint64_t)16 * S, (cuuint64_t)16 * S * S, (cuuint64_t)16 * S * S * S};
+  cuuint32_t box[4] = {4 * HX, HY, HZ, (cuuint32_t)A.cqc};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)in, gdim, gstride, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   MDP_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d) for S=%d cin=%d", (int)r, S, cin);
 
-  const size_t smem = 1024 + (size_t)A.na * A.a_bytes + (size_t)nbs * A.b_bytes + 1024;
+  const size_t smem = 1024 + (size_t)A.na * A.a_bytes + (size_t)nbs * A.b_bytes + 2048;
   static size_t attr_set = 0;
   if (attr_set < smem) {
     cudaFuncSetAttribute(conv3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));

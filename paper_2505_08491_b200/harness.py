@@ -21,7 +21,7 @@ import numpy as np
 from . import _ext
 from .assembly import CoupledSystem, DeviceProblem, full_rhs, one_d_operator
 from .geometry import DistanceField, distance_field_device
-from .krylov import DeviceIlu, FgmresEngine, IluPreconditioner, SolveReport, ilu0
+from .krylov import DeviceIlu, FgmresEngine, FixedStepFgmres, IluPreconditioner, SolveReport, ilu0
 from .neural import PATH_TCGEN05, UNetParams, device_net, load_checkpoint
 from .operators import CoupledOperator, CouplingOps, ReducedOperator
 from .training import BatchedNeural, NeuralPreconditioner
@@ -68,7 +68,7 @@ def mesh_distance(system: CoupledSystem):
 class CoupledSolver:
     """Device state for repeated coupled solves of a batch of systems."""
 
-    def __init__(self, systems, strategy: CoupledStrategy, path: int = PATH_TCGEN05):
+    def __init__(self, systems, strategy: CoupledStrategy, path: int = PATH_TCGEN05, graphs: bool = True):
         import torch
         if strategy.one_d != "ilu0":
             raise ValueError("the device path implements the one_d='ilu0' strategy")
@@ -100,6 +100,8 @@ class CoupledSolver:
             raise ValueError(f"inner preconditioner {kind!r} is not on the device hot path")
         self.outer = FgmresEngine(p.nsys, p.n3 + p.n1max, p.ld, strategy.restart)
         self.inner_eng = FgmresEngine(p.nsys, p.n3, p.ld, strategy.inner_iterations)
+        self.fixed = FixedStepFgmres(p.nsys, p.n3, p.ld, strategy.inner_iterations)
+        self.graphs = graphs
         self.b3 = p.zeros()
         self.F = p.pack([full_rhs(s) for s in self.systems])
 
@@ -122,11 +124,33 @@ class CoupledSolver:
         _ext.check(self.lib.mdp_copy_vec(m, sel.data_ptr(), self.inner_eng.x.data_ptr(), p.ld, Z.data_ptr(), p.ld,
                                          None, 0, n3, _ext.stream()))
 
+    def _block_precond_graph(self, V, Z, sel, idx, flag):
+        """Graph-safe block preconditioner: same pieces, inner solve fully on device.
+
+        Writes flag[i] != 0 for systems whose inner solve hit a breakdown or
+        a zero right-hand side; the outer engine re-runs those through the
+        exact ``_block_precond``.
+        """
+        p = self.prob
+        m = int(sel.numel())
+        n3 = p.n3
+        _ext.check(self.lib.mdp_ilu0_apply(self.ilu.desc, m, sel.data_ptr(), V.data_ptr() + 8 * n3,
+                                           Z.data_ptr() + 8 * n3, p.ld, _ext.stream()))
+        _ext.check(self.lib.mdp_copy_vec(m, sel.data_ptr(), V.data_ptr(), p.ld, self.b3.data_ptr(), p.ld, None, 0,
+                                         n3, _ext.stream()))
+        self.cpl.minus_w_m01(Z, self.b3, sel)
+        P = self.inner.apply_device if self.inner is not None else None
+        self.fixed.run(self.C.matvec, P, self.b3, sel, idx)
+        _ext.check(self.lib.mdp_copy_vec(m, sel.data_ptr(), self.fixed.x.data_ptr(), p.ld, Z.data_ptr(), p.ld,
+                                         None, 0, n3, _ext.stream()))
+        flag[:m].copy_(self.fixed.flag[:m])
+
     def solve(self, F=None):
         """Outer FGMRES (harness.py:394-395); returns per-system reports, x left on device."""
         st = self.st
         return self.outer.solve(self.A.matvec, self._block_precond, self.F if F is None else F,
-                                tol=st.tol, maxit=st.maxit)
+                                tol=st.tol, maxit=st.maxit,
+                                Pg=self._block_precond_graph if self.graphs else None)
 
     def solution(self):
         out = []

@@ -108,21 +108,26 @@ class FgmresEngine:
         self.vcur = torch.zeros((nsys, ld), **f)
         self.zcur = torch.zeros((nsys, ld), **f)
         self.tmp = torch.zeros((nsys, ld), **f)
-        self.hcol = torch.zeros((nsys, restart + 2), **f)
+        # Hessenberg columns [nsys][k+2] followed by one flag per system (graph steps)
+        self.hbuf = torch.zeros(nsys * (restart + 2) + nsys, **f)
+        self.hcol = self.hbuf[:nsys * (restart + 2)].view(nsys, restart + 2)
+        self.pflag = self.hbuf[nsys * (restart + 2):]
+        self._graphs = {}
+        self.replayed_kernels = 0  # our kernels executed through graph replays
         self.rn = torch.zeros(nsys, **f)
         self.ybuf = torch.zeros((nsys, restart), **f)
         self.betad = torch.zeros(nsys, **f)
-        wb = max(self.lib.mdp_arnoldi_work_bytes(nsys, restart, n), 8 * nsys * 1024)
-        self.work = torch.empty(wb // 8 + 1, **f)
+        wb = self.lib.mdp_arnoldi_work_bytes(nsys, restart, n)
+        self.work = torch.zeros(wb // 8 + 1, **f)  # reduction tickets must start at zero
         pin = dict(pin_memory=True)
-        self.h_host = torch.zeros((nsys, restart + 2), dtype=torch.float64, **pin)
+        self.h_host = torch.zeros(nsys * (restart + 2) + nsys, dtype=torch.float64, **pin)
         self.rn_host = torch.zeros(nsys, dtype=torch.float64, **pin)
         self.y_host = torch.zeros((nsys, restart), dtype=torch.float64, **pin)
         self.beta_host = torch.zeros(nsys, dtype=torch.float64, **pin)
         # one pinned staging slot + device copy per upload purpose: a slot is
         # rewritten only after a stream synchronisation since its last copy
         self._regions = {}
-        for name in ("all", "start", "arn", "js", "nv", "end", "cnt", "res"):
+        for name in ("all", "start", "arn", "js", "nv", "end", "cnt", "res", "redo", "rjs", "rnv"):
             self._regions[name] = (torch.zeros(nsys, dtype=torch.int32, pin_memory=True),
                                    torch.zeros(nsys, dtype=torch.int32, device=device))
 
@@ -135,6 +140,62 @@ class FgmresEngine:
         host[:m] = torch.as_tensor(np.asarray(values, dtype=np.int32))
         dev[:m].copy_(host[:m], non_blocking=True)
         return dev[:m]
+
+    def _step(self, A, P, sel, jd, nv, ma, idx):
+        """Z[j] = P(V[j]); w = A Z[j]; CGS2 projections; V[j+1] = w/||w|| (krylov.py:136-141, 165)."""
+        k = self.k
+        if P is None:
+            _ext.check(self.lib.mdp_copy_vec(ma, sel.data_ptr(), self.vcur.data_ptr(), self.ld,
+                                             self.zcur.data_ptr(), self.ld, None, 0, self.n, _ext.stream()))
+        else:
+            P(self.vcur, self.zcur, sel, idx)
+        _ext.check(self.lib.mdp_copy_vec(ma, sel.data_ptr(), self.zcur.data_ptr(), self.ld,
+                                         self.Z.data_ptr(), k * self.ld, jd.data_ptr(), self.ld, self.n,
+                                         _ext.stream()))
+        A(self.zcur, self.w, sel)
+        _ext.check(self.lib.mdp_arnoldi(ma, sel.data_ptr(), self.V.data_ptr(), (k + 1) * self.ld, self.ld,
+                                        nv.data_ptr(), k, self.w.data_ptr(), self.ld, self.n,
+                                        self.hcol.data_ptr(), self.vcur.data_ptr(), self.ld,
+                                        self.work.data_ptr(), _ext.stream()))
+
+    def _capture(self, A, Pg, sel, jd, nv, ma, idx):
+        """CUDA graph of one Arnoldi step with a graph-safe preconditioner.
+
+        Pg(V, Z, sel, idx, flag) must not allocate or synchronise and
+        writes a nonzero flag for any system it could not handle exactly.
+        """
+        import torch
+
+        def P(V, Z, sel_, idx_):
+            Pg(V, Z, sel_, idx_, self.pflag)
+
+        # eager warm-up (first-use setup outside capture), then restore vcur = V[j]
+        self._step(A, P, sel, jd, nv, ma, idx)
+        self._gather_slot(sel, jd, ma)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        l0 = self.lib.mdp_launch_count()
+        with torch.cuda.graph(g):
+            self._step(A, P, sel, jd, nv, ma, idx)
+        return g, self.lib.mdp_launch_count() - l0
+
+    def _gather_slot(self, sel, jd, m):
+        """vcur_s = V[s, j_s] for the listed systems."""
+        k = self.k
+        _ext.check(self.lib.mdp_copy_slot(m, sel.data_ptr(), self.V.data_ptr(), (k + 1) * self.ld, jd.data_ptr(),
+                                          self.ld, self.vcur.data_ptr(), self.ld, self.n, _ext.stream()))
+
+    def _read_h(self, m, with_flags=False):
+        import torch
+        kk = self.k + 2
+        nf = self.nsys * kk
+        self.h_host[:m * kk].copy_(self.hbuf[:m * kk], non_blocking=True)
+        if with_flags:
+            self.h_host[nf:nf + m].copy_(self.pflag[:m], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        h = self.h_host[:m * kk].numpy().reshape(m, kk)
+        f = self.h_host[nf:nf + m].numpy() if with_flags else None
+        return h, f
 
     def _sync_read(self, dev, host, m):
         import torch
@@ -152,14 +213,17 @@ class FgmresEngine:
 
     # -- the solve -----------------------------------------------------------------
     def solve(self, A, P, b, tol: float = 1e-6, maxit: int = 1000, x0=None, systems=None,
-              final_residual: bool = True):
+              final_residual: bool = True, Pg=None):
         """Solve A x = b for the listed systems (default all); returns reports.
 
         ``b`` is an (nsys, ld) storage; ``x0`` an optional storage.  The
         solution is left in ``self.x``.  ``final_residual=False`` skips the
         last cycle's true-residual computation when no further cycle can
         follow (inner solves whose report is discarded, harness.py:385-387);
-        the returned x is unaffected.
+        the returned x is unaffected.  ``Pg``: optional graph-safe variant
+        of ``P`` (see ``_capture``); the Arnoldi step then runs as one CUDA
+        graph per set of active systems, falling back to ``P`` for flagged
+        systems.
         """
         import torch
         if tol <= 0:
@@ -233,22 +297,34 @@ class FgmresEngine:
             jd = self._upload("js", js)
             nv = self._upload("nv", [j + 1 for j in js])
             ma = len(arn)
-            if P is None:
-                _ext.check(self.lib.mdp_copy_vec(ma, sel.data_ptr(), self.vcur.data_ptr(), self.ld,
-                                                 self.zcur.data_ptr(), self.ld, None, 0, self.n, _ext.stream()))
+            if Pg is not None:
+                key = tuple(arn)
+                g = self._graphs.get(key)
+                if g is None:
+                    g = self._capture(A, Pg, sel, jd, nv, ma, arn)
+                    self._graphs[key] = g
+                g[0].replay()
+                self.replayed_kernels += g[1]
+                hb = self._read_h(ma, with_flags=True)
+                redo = [s for i, s in enumerate(arn) if hb[1][i] != 0.0]
+                if redo:
+                    # exact host-driven path for systems whose graph step hit a flagged case
+                    rsel = self._upload("redo", redo)
+                    rj = self._upload("rjs", [st[s].j for s in redo])
+                    rnv = self._upload("rnv", [st[s].j + 1 for s in redo])
+                    # the graph overwrote vcur with V[j+1]; restore V[j] for the redo
+                    self._gather_slot(rsel, rj, len(redo))
+                    self._step(A, P, rsel, rj, rnv, len(redo), redo)
+                    hr = self._read_h(len(redo))[0]
+                    pos = {s: i for i, s in enumerate(arn)}
+                    hc = hb[0].copy()
+                    for i, s in enumerate(redo):
+                        hc[pos[s]] = hr[i]
+                else:
+                    hc = hb[0]
             else:
-                P(self.vcur, self.zcur, sel, arn)
-            # Z[j] = z
-            _ext.check(self.lib.mdp_copy_vec(ma, sel.data_ptr(), self.zcur.data_ptr(), self.ld,
-                                             self.Z.data_ptr(), k * self.ld, jd.data_ptr(), self.ld, self.n,
-                                             _ext.stream()))
-            A(self.zcur, self.w, sel)
-            # nv = j + 1 projections; V[j+1] = w / ||w|| written on device (also vcur)
-            _ext.check(self.lib.mdp_arnoldi(ma, sel.data_ptr(), self.V.data_ptr(), (k + 1) * self.ld, self.ld,
-                                            nv.data_ptr(), k, self.w.data_ptr(), self.ld, self.n,
-                                            self.hcol.data_ptr(), self.vcur.data_ptr(), self.ld,
-                                            self.work.data_ptr(), _ext.stream()))
-            hc = self._sync_read(self.hcol, self.h_host, ma)
+                self._step(A, P, sel, jd, nv, ma, arn)
+                hc = self._read_h(ma)[0]
             ending = []
             for i, s in enumerate(arn):
                 S = st[s]
@@ -343,6 +419,76 @@ class FgmresEngine:
                 S.conv = True
             if S.conv or S.iters >= maxit:
                 self._finish(S)
+
+
+class FixedStepFgmres:
+    """FGMRES with restart = maxit = m and tol = 1e-300, entirely on the device.
+
+    This is the inner 3D solve of the block preconditioner
+    (harness.py:385-387): with a tolerance of 1e-300 its control flow is
+    static -- exactly m Arnoldi steps, then x = Z y -- unless an Arnoldi
+    breakdown occurs or the right-hand side is zero.  The Givens rotations
+    and the back substitution run in tiny device kernels (mdp_givens_step,
+    mdp_backsub) so the whole solve can be captured in a CUDA graph; any
+    system that hits a breakdown / zero rhs raises its flag and must be
+    re-solved by the host-driven ``FgmresEngine`` (which reproduces
+    krylov.fgmres branch by branch).
+    """
+
+    def __init__(self, nsys: int, n: int, ld: int, m: int, device="cuda"):
+        import torch
+        self.lib = _ext.lib()
+        self.nsys, self.n, self.ld, self.k = nsys, n, ld, m
+        f = dict(dtype=torch.float64, device=device)
+        self.V = torch.zeros((nsys, m + 1, ld), **f)
+        self.Z = torch.zeros((nsys, m, ld), **f)
+        self.x = torch.zeros((nsys, ld), **f)
+        self.w = torch.zeros((nsys, ld), **f)
+        self.vcur = torch.zeros((nsys, ld), **f)
+        self.zcur = torch.zeros((nsys, ld), **f)
+        self.hcol = torch.zeros((nsys, m + 2), **f)
+        self.H = torch.zeros((nsys, m + 1, m), **f)
+        self.cs = torch.zeros((nsys, m), **f)
+        self.sn = torch.zeros((nsys, m), **f)
+        self.g = torch.zeros((nsys, m + 1), **f)
+        self.y = torch.zeros((nsys, m), **f)
+        self.beta = torch.zeros(nsys, **f)
+        self.flag = torch.zeros(nsys, **f)
+        self.nvs = [torch.full((nsys,), j + 1, dtype=torch.int32, device=device) for j in range(m)]
+        self.cnt = torch.full((nsys,), m, dtype=torch.int32, device=device)
+        wb = self.lib.mdp_arnoldi_work_bytes(nsys, m, n)
+        self.work = torch.zeros(wb // 8 + 1, **f)  # reduction tickets must start at zero
+
+    def run(self, A, P, b, sel, idx):
+        """Enqueue the solve of A x = b for the selected systems (no host sync)."""
+        L, st = self.lib, _ext.stream()
+        m, k, ld, n = int(sel.numel()), self.k, self.ld, self.n
+        sp_ = sel.data_ptr()
+        _ext.check(L.mdp_norms(m, sp_, b.data_ptr(), ld, n, self.beta.data_ptr(), self.work.data_ptr(), st))
+        _ext.check(L.mdp_fixed_init(m, k, self.beta.data_ptr(), self.H.data_ptr(), self.cs.data_ptr(),
+                                    self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), st))
+        V0 = self.V[:, 0, :]
+        _ext.check(L.mdp_scale(m, sp_, b.data_ptr(), ld, None, self.beta.data_ptr(), V0.data_ptr(), (k + 1) * ld, n,
+                               st))
+        _ext.check(L.mdp_copy_vec(m, sp_, V0.data_ptr(), (k + 1) * ld, self.vcur.data_ptr(), ld, None, 0, n, st))
+        for j in range(k):
+            if P is None:
+                _ext.check(L.mdp_copy_vec(m, sp_, self.vcur.data_ptr(), ld, self.zcur.data_ptr(), ld, None, 0, n, st))
+            else:
+                P(self.vcur, self.zcur, sel, idx)
+            Zj = self.Z[:, j, :]
+            _ext.check(L.mdp_copy_vec(m, sp_, self.zcur.data_ptr(), ld, Zj.data_ptr(), k * ld, None, 0, n, st))
+            A(self.zcur, self.w, sel)
+            _ext.check(L.mdp_arnoldi(m, sp_, self.V.data_ptr(), (k + 1) * ld, ld, self.nvs[j].data_ptr(), k,
+                                     self.w.data_ptr(), ld, n, self.hcol.data_ptr(), self.vcur.data_ptr(), ld,
+                                     self.work.data_ptr(), st))
+            _ext.check(L.mdp_givens_step(m, k, j, self.hcol.data_ptr(), self.H.data_ptr(), self.cs.data_ptr(),
+                                         self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), st))
+        _ext.check(L.mdp_backsub(m, k, k, self.H.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(),
+                                 self.y.data_ptr(), st))
+        _ext.check(L.mdp_fill(m, sp_, self.x.data_ptr(), ld, n, 0.0, st))
+        _ext.check(L.mdp_basis_update(m, sp_, self.x.data_ptr(), ld, self.Z.data_ptr(), k * ld, ld,
+                                      self.cnt.data_ptr(), self.y.data_ptr(), k, n, st))
 
 
 # ---------------------------------------------------------------------------
@@ -466,7 +612,7 @@ class DeviceIlu:
         for i, f in enumerate(factors):
             lev_f[i, :f.nlev_f + 1] = f.lev_f[:f.nlev_f + 1]
             lev_b[i, :f.nlev_b + 1] = f.lev_b[:f.nlev_b + 1]
-        if max(rows) > 8000:
+        if max(rows) > 25000:
             raise ValueError("1D block too large for the single-CTA ILU sweep (shared memory)")
         T = lambda a, dt=torch.int32: torch.as_tensor(np.ascontiguousarray(a).ravel(), dtype=dt, device=device)  # noqa: E731
         self._t = dict(row_start=T(row_start), ptr=T(ptr), col=T(col), val=T(val, torch.float64), diag=T(diag),
@@ -475,6 +621,7 @@ class DeviceIlu:
                        nlev_f=T([f.nlev_f for f in factors]), nlev_b=T([f.nlev_b for f in factors]))
         d = _ext.MdpIlu()
         d.nsys, d.lev_stride = nsys, stride
+        d.max_rows, d.max_nnz = max(rows), max(nnz)
         for key, t in self._t.items():
             setattr(d, key, t.data_ptr())
         self.desc = d

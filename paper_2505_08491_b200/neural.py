@@ -9,7 +9,7 @@ seeds give the reference's weights), MDU3 ``save_checkpoint`` /
 Weights are uploaded once as float32 in kernel-specific packed layouts:
 
   path 0 (tcgen05 TF32, product):  3^3 conv [chunk][tap][quad][Cout][4],
-      chunk = 32 input channels (16 for Cin=16), values rounded to TF32;
+      chunk = 16 input channels, values rounded to TF32;
   path 1 (CUDA-core FP32, check):  3^3 conv [Cout/16][Cin][27][16];
   both: enc1a [16][2][27], tconv [Cout/16][Cin][8][16], head1 [16][32],
       head2 [16].
@@ -168,7 +168,7 @@ def pack_conv(kernel: np.ndarray, path: int) -> np.ndarray:
     k = np.asarray(kernel, dtype=np.float32).reshape(cout, cin, 27)
     if path == PATH_CUDA_CORE:
         return np.ascontiguousarray(k.reshape(cout // 16, 16, cin, 27).transpose(0, 2, 3, 1))
-    cqc = 8 if cin >= 32 else cin // 4
+    cqc = 4  # 16-channel chunks (unet_tc.cu)
     nch = cin // (4 * cqc)
     p = k.reshape(cout, nch, cqc, 4, 27).transpose(1, 4, 2, 0, 3)  # [chunk][tap][quad][cout][4]
     return tf32_round(np.ascontiguousarray(p))
@@ -213,15 +213,19 @@ class DeviceUNet:
             else:
                 d.b[i] = None
         self.desc = d
-        self._ws = {}
+        self._ws = None
+        self._old = []
 
     def workspace(self, n: int, nb: int):
+        """Grow-only activation workspace (a captured CUDA graph may hold the
+        current buffer, so it is never freed while this object lives)."""
         import torch
-        key = (n, nb)
-        if key not in self._ws:
-            nbytes = self.lib.mdp_unet_workspace_bytes(n, nb, self.path)
-            self._ws = {key: torch.empty(nbytes, dtype=torch.uint8, device=self.device)}
-        return self._ws[key]
+        nbytes = self.lib.mdp_unet_workspace_bytes(n, nb, self.path)
+        if self._ws is None or self._ws.numel() < nbytes:
+            if self._ws is not None:
+                self._old.append(self._ws)
+            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self._ws
 
     def apply(self, n: int, R, ld: int, rnorm, D, ldd: int, Z, ldz: int, sel=None, nb=None):
         """Z_s = rnorm_i * U([R_s / rnorm_i | D_s]) for the selected systems."""

@@ -39,7 +39,8 @@ class BatchedNeural:
             self.D.copy_(dists)
         f = dict(dtype=torch.float64, device=dev)
         self.rn = torch.zeros(nsys, **f)
-        self.work = torch.zeros(4 * 148 * nsys + 1024, **f)
+        self.lib = _ext.lib()
+        self.work = torch.zeros(self.lib.mdp_arnoldi_work_bytes(nsys, 1, self.n3) // 8 + 1, **f)
         if smoothing is not None:
             self.t1 = torch.zeros((nsys, ld), **f)
             self.t2 = torch.zeros((nsys, ld), **f)

@@ -95,8 +95,8 @@ def test_weight_packing_layouts():
     k = rng.standard_normal((64, 32, 3, 3, 3)).astype(np.float32)
     p1 = neural.pack_conv(k, neural.PATH_CUDA_CORE).reshape(4, 32, 27, 16)
     assert p1[1, 5, 13, 7] == k[16 + 7, 5].ravel()[13]
-    p0 = neural.pack_conv(k, neural.PATH_TCGEN05).reshape(1, 27, 8, 64, 4)
-    assert abs(p0[0, 13, 2, 40, 3] - k[40, 2 * 4 + 3].ravel()[13]) <= 2e-3 * abs(k[40, 11].ravel()[13])
+    p0 = neural.pack_conv(k, neural.PATH_TCGEN05).reshape(2, 27, 4, 64, 4)
+    assert abs(p0[1, 13, 2, 40, 3] - k[40, 16 + 2 * 4 + 3].ravel()[13]) <= 2e-3 * abs(k[40, 27].ravel()[13])
     t = rng.standard_normal((64, 32, 2, 2, 2)).astype(np.float32)
     pt = neural.pack_tconv(t).reshape(2, 64, 8, 16)
     assert pt[1, 10, 5, 3] == t[10, 16 + 3].ravel()[5]

@@ -197,7 +197,7 @@ def test_arnoldi_kernel_orthogonalises(gpu):
     W = torch.as_tensor(wv, device="cuda").reshape(1, n).clone()
     nv = torch.tensor([k], dtype=torch.int32, device="cuda")
     H = torch.zeros((1, k + 2), dtype=torch.float64, device="cuda")
-    work = torch.empty(lib.mdp_arnoldi_work_bytes(1, k, n) // 8 + 1, dtype=torch.float64, device="cuda")
+    work = torch.zeros(lib.mdp_arnoldi_work_bytes(1, k, n) // 8 + 1, dtype=torch.float64, device="cuda")
     _ext.check(lib.mdp_arnoldi(1, None, V.data_ptr(), (k + 1) * n, n, nv.data_ptr(), k, W.data_ptr(), n, n,
                                H.data_ptr(), None, 0, work.data_ptr(), _ext.stream()))
     h = H[0].cpu().numpy()
