@@ -139,12 +139,12 @@ __device__ __forceinline__ void issue_stage(uint32_t a_lo, uint32_t a_hi, uint32
     for (int ks = 0; ks < 2; ++ks) {
       const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo + tt * b_tap16 + ks * b_ks16);
 #pragma unroll
-      for (int zp = 0; zp < ZP; ++zp) {
+      for (int zp = 0; zp < ZP; ++zp) {  // one accumulator per z-plane
         const uint32_t off = tap_off16(tt) + (uint32_t)(zp * HY * HX) + (uint32_t)(ks * 2 * (QUAD_BYTES / 16));
         const uint64_t ad = ((uint64_t)a_hi << 32) | (a_lo + off);
         mma_tf32(dcol + zp * ncol, ad, bd, idesc, accf);
-        accf = 1u;
       }
+      accf = 1u;
     }
   }
 }
