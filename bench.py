@@ -145,11 +145,12 @@ def conv_layer_times(n, reps=20):
                             device="cuda")
         So = S // 2 if pool else S
         Y = torch.empty(cout * So ** 3, dtype=torch.float32, device="cuda")
+        scr = torch.empty(max(lib.mdp_conv3_scratch_bytes(1, S, cin, cout), 16), dtype=torch.uint8, device="cuda")
         st = _ext.stream()
 
         def run():
             _ext.check(lib.mdp_conv3_layer(0, 1, S, cin, cout, X.data_ptr(), cin // 4, 0, W.data_ptr(), None, 1,
-                                           Y.data_ptr(), cout // 4, 0, pool, st))
+                                           Y.data_ptr(), cout // 4, 0, pool, scr.data_ptr(), scr.numel(), st))
         run()
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -230,7 +230,9 @@ int mdp_unet_apply(const mdp_unet* net, int32_t nb, const int32_t* sel, const do
 int mdp_conv3_layer(int32_t path, int32_t nb, int32_t S, int32_t cin, int32_t cout,
                     const float* in, int32_t in_cq, int32_t in_q0, const float* w, const float* bias,
                     int32_t relu, float* out, int32_t out_cq, int32_t out_q0, int32_t pool,
-                    void* stream);
+                    void* scratch, size_t scratch_bytes, void* stream);
+/* Scratch bytes mdp_conv3_layer (path 0) needs for split-K partial sums. */
+size_t mdp_conv3_scratch_bytes(int32_t nb, int32_t S, int32_t cin, int32_t cout);
 
 /* ------------------------------------------------------------------ */
 const char* mdp_last_error(void);

@@ -71,7 +71,8 @@ _SIGS = {
     "mdp_unet_apply": (_i32, [C.POINTER(MdpUnet), _i32, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _i64,
                               _vp, C.c_size_t, _vp]),
     "mdp_conv3_layer": (_i32, [_i32, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp, _i32, _vp,
-                               _i32, _i32, _i32, _vp]),
+                               _i32, _i32, _i32, _vp, C.c_size_t, _vp]),
+    "mdp_conv3_scratch_bytes": (C.c_size_t, [_i32, _i32, _i32, _i32]),
     "mdp_last_error": (C.c_char_p, []),
     "mdp_version": (_i32, []),
     "mdp_launch_count": (C.c_longlong, []),

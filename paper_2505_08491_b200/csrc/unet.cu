@@ -295,8 +295,17 @@ UnetPlan unet_plan(int n, int nb, int path) {
   if (path == 1) {  // unfused pooling needs the full-resolution pre-pool tensors
     p.o_e2 = take((size_t)nb * 16 * N * 16);
     p.o_e3 = take((size_t)nb * 32 * M * 16);
+    p.o_scr = p.scr_bytes = 0;
   } else {
     p.o_e2 = p.o_e3 = 0;
+    size_t scr = 0;
+    const int shp[6][3] = {{n, 16, 32}, {n, 32, 64}, {p.m, 64, 128}, {p.q, 128, 128}, {p.m, 128, 64}, {n, 64, 32}};
+    for (auto& L : shp) {
+      size_t b = tc_conv3_scratch_bytes(nb, L[0], L[1], L[2]);
+      scr = b > scr ? b : scr;
+    }
+    p.scr_bytes = scr;
+    p.o_scr = scr ? take(scr) : 0;
   }
   p.bytes = off;
   return p;
@@ -310,9 +319,14 @@ extern "C" size_t mdp_unet_workspace_bytes(int32_t n, int32_t nb, int32_t path) 
   return unet_plan(n, nb, path).bytes;
 }
 
+extern "C" size_t mdp_conv3_scratch_bytes(int32_t nb, int32_t S, int32_t cin, int32_t cout) {
+  return tc_conv3_scratch_bytes(nb, S, cin, cout);
+}
+
 extern "C" int mdp_conv3_layer(int32_t path, int32_t nb, int32_t S, int32_t cin, int32_t cout, const float* in,
                                int32_t in_cq, int32_t in_q0, const float* w, const float* bias, int32_t relu,
-                               float* out, int32_t out_cq, int32_t out_q0, int32_t pool, void* stream) {
+                               float* out, int32_t out_cq, int32_t out_q0, int32_t pool, void* scratch,
+                               size_t scratch_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (path == 1) {
     MDP_REQUIRE(!pool, "direct path conv layer has no fused pool");
@@ -320,7 +334,7 @@ extern "C" int mdp_conv3_layer(int32_t path, int32_t nb, int32_t S, int32_t cin,
                        out_q0, st);
   }
   return tc_conv3(nb, S, cin, cout, (const float4*)in, in_cq, in_q0, w, bias, relu, (float4*)out, out_cq, out_q0,
-                  pool ? EPI_POOL : EPI_STORE, nullptr, st);
+                  pool ? EPI_POOL : EPI_STORE, nullptr, scratch, scratch_bytes, st);
 }
 
 extern "C" int mdp_unet_apply(const mdp_unet* net, int32_t nb, const int32_t* sel, const double* r, int64_t ld,
@@ -372,19 +386,19 @@ extern "C" int mdp_unet_apply(const mdp_unet* net, int32_t nb, const int32_t* se
     if ((rc = launch_tconv(nb, d2, 16, 64, 32, m, op1, net->w[7], net->b[7], c1, 16, 0, 0, st))) return rc;
     if ((rc = direct_conv(nb, n, 64, 32, c1, 16, 0, net->w[8], net->b[8], 1, d1, 8, 0, st))) return rc;
   } else {
-    if ((rc = tc_conv3(nb, n, 16, 32, a1, 4, 0, net->w[1], net->b[1], 1, c1, 16, 8, EPI_STORE, nullptr, st)))
+    if ((rc = tc_conv3(nb, n, 16, 32, a1, 4, 0, net->w[1], net->b[1], 1, c1, 16, 8, EPI_STORE, nullptr, ws + P.o_scr, P.scr_bytes, st)))
       return rc;
-    if ((rc = tc_conv3(nb, n, 32, 64, c1, 16, 8, net->w[2], nullptr, 1, c2, 32, 16, EPI_POOL, nullptr, st)))
+    if ((rc = tc_conv3(nb, n, 32, 64, c1, 16, 8, net->w[2], nullptr, 1, c2, 32, 16, EPI_POOL, nullptr, ws + P.o_scr, P.scr_bytes, st)))
       return rc;
-    if ((rc = tc_conv3(nb, m, 64, 128, c2, 32, 16, net->w[3], nullptr, 1, p2, 32, 0, EPI_POOL, nullptr, st)))
+    if ((rc = tc_conv3(nb, m, 64, 128, c2, 32, 16, net->w[3], nullptr, 1, p2, 32, 0, EPI_POOL, nullptr, ws + P.o_scr, P.scr_bytes, st)))
       return rc;
-    if ((rc = tc_conv3(nb, q, 128, 128, p2, 32, 0, net->w[4], nullptr, 1, bt, 32, 0, EPI_STORE, nullptr, st)))
+    if ((rc = tc_conv3(nb, q, 128, 128, p2, 32, 0, net->w[4], nullptr, 1, bt, 32, 0, EPI_STORE, nullptr, ws + P.o_scr, P.scr_bytes, st)))
       return rc;
     if ((rc = launch_tconv(nb, bt, 32, 128, 64, q, op2, net->w[5], nullptr, c2, 32, 0, 1, st))) return rc;
-    if ((rc = tc_conv3(nb, m, 128, 64, c2, 32, 0, net->w[6], net->b[6], 1, d2, 16, 0, EPI_STORE, nullptr, st)))
+    if ((rc = tc_conv3(nb, m, 128, 64, c2, 32, 0, net->w[6], net->b[6], 1, d2, 16, 0, EPI_STORE, nullptr, ws + P.o_scr, P.scr_bytes, st)))
       return rc;
     if ((rc = launch_tconv(nb, d2, 16, 64, 32, m, op1, net->w[7], net->b[7], c1, 16, 0, 1, st))) return rc;
-    if ((rc = tc_conv3(nb, n, 64, 32, c1, 16, 0, net->w[8], net->b[8], 1, d1, 8, 0, EPI_STORE, nullptr, st)))
+    if ((rc = tc_conv3(nb, n, 64, 32, c1, 16, 0, net->w[8], net->b[8], 1, d1, 8, 0, EPI_STORE, nullptr, ws + P.o_scr, P.scr_bytes, st)))
       return rc;
   }
   head_kernel<<<dim3(ceil_div(N, 128), nb), 128, 0, st>>>(d1, n, net->w[9], net->b[9], net->w[10], net->b[10],

@@ -7,7 +7,7 @@ namespace mdp {
 
 struct UnetPlan {
   int n, m, q;
-  size_t o_xin, o_a1, o_c1, o_c2, o_p2, o_bt, o_d2, o_d1, o_e2, o_e3;
+  size_t o_xin, o_a1, o_c1, o_c2, o_p2, o_bt, o_d2, o_d1, o_e2, o_e3, o_scr, scr_bytes;
   size_t bytes;
 };
 UnetPlan unet_plan(int n, int nb, int path);
@@ -29,7 +29,9 @@ struct HeadArgs {  // dec1 -> head1 -> head2 -> scale (EPI_HEAD)
 // w packed by paper_2505_08491_b200.neural.pack_tc.
 int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int in_q0, const float* w,
              const float* bias, int relu, float4* out, int out_cq, int out_q0, int epi, const HeadArgs* head,
-             cudaStream_t st);
+             void* scratch, size_t scratch_bytes, cudaStream_t st);
+// scratch needed by the split-K partial sums of one layer (0 when not split)
+size_t tc_conv3_scratch_bytes(int nb, int S, int cin, int cout);
 
 __device__ __forceinline__ float tf32_round(float f) {
   uint32_t u;

@@ -40,6 +40,8 @@ constexpr int QUAD_BYTES = HROWS * 16;
 struct ConvArgs {
   int nb, S, cin, cout, cqc, nchunk;
   int nsplit, ncol;  // output channels split over nsplit CTAs of ncol each (small layers)
+  int ksplit, cps;   // input-channel chunks split over ksplit CTAs of cps chunks (small layers)
+  float4* partial;   // ksplit > 1: raw FP32 partial sums [ks][item][Cout/4][S^3]
   int tx, ty, tz, ntiles;
   int in_cq, in_q0;
   const float* w;
@@ -173,9 +175,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 }
 
 __device__ __forceinline__ void decode_tile(const ConvArgs& A, int tile, int& b, int& x0, int& y0, int& z0,
-                                            int& n0) {
+                                            int& n0, int& ks) {
   n0 = (tile % A.nsplit) * A.ncol;
   tile /= A.nsplit;
+  ks = tile % A.ksplit;
+  tile /= A.ksplit;
   int ix = tile % A.tx;
   int t = tile / A.tx;
   int iy = t % A.ty;
@@ -234,9 +238,9 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
     if (lane == 0) {  // ---------------- A producer: halo bricks, one TMA box per 32-channel chunk
       int as = 0, ap = 0;
       for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
-        int b, x0, y0, z0, n0;
-        decode_tile(A, tile, b, x0, y0, z0, n0);
-        for (int c = 0; c < A.nchunk; ++c) {
+        int b, x0, y0, z0, n0, ks;
+        decode_tile(A, tile, b, x0, y0, z0, n0, ks);
+        for (int c = ks * A.cps; c < (ks + 1) * A.cps; ++c) {
           mbar_wait(&a_empty[as], ap ^ 1);
           if (A.dbg & 4) {
             mbar_arrive(&a_full[as]);
@@ -255,9 +259,9 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
       int bs = 0, bp = 0;
       for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
         if (A.resident && tile != (int)blockIdx.x) break;  // resident filter: loaded once
-        int b, x0, y0, z0, n0;
-        decode_tile(A, tile, b, x0, y0, z0, n0);
-        for (int c = 0; c < A.nchunk; ++c) {
+        int b, x0, y0, z0, n0, ks;
+        decode_tile(A, tile, b, x0, y0, z0, n0, ks);
+        for (int c = ks * A.cps; c < (ks + 1) * A.cps; ++c) {
           // packed weights [chunk][tap][quad][cout][4]; a stage holds tps
           // consecutive taps: one contiguous copy when the CTA owns every
           // output channel, else one per (tap, quad)
@@ -301,7 +305,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
         fence_after();
         const uint32_t dcol = tmem + (uint32_t)(buf * ZP * A.ncol);
         uint32_t accf = 0u;  // the tile's first MMA overwrites the accumulator
-        for (int c = 0; c < A.nchunk; ++c) {
+        for (int c = 0; c < A.cps; ++c) {
           mbar_wait(&a_full[as], ap);
           fence_after();
           const uint32_t abase = a0 + as * A.a_bytes;
@@ -345,14 +349,31 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
     int li = 0;
     for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++li) {
       const int buf = li & 1;
-      int b, x0, y0, z0, n0;
-      decode_tile(A, tile, b, x0, y0, z0, n0);
+      int b, x0, y0, z0, n0, ks;
+      decode_tile(A, tile, b, x0, y0, z0, n0, ks);
       mbar_wait(&t_full[buf], (li >> 1) & 1);
       fence_after();
       const uint32_t dcol = tmem + lane_addr + (uint32_t)(buf * ZP * A.ncol);
       const int q0 = A.out_q0 + n0 / 4;
       const int gx = x0 + lx, gy = y0 + ly;
-      if (A.epi == EPI_POOL) {
+      if (A.ksplit > 1) {  // raw partial sums; conv_split_reduce_kernel finishes the layer
+#pragma unroll
+        for (int zp = 0; zp < ZP; ++zp) {
+          const int gz = z0 + zp;
+          const bool ok = gx < S && gy < S && gz < S;
+          for (int cg = 0; cg < A.ncol / 16; ++cg) {
+            float v[16];
+            tmem_ld16(dcol + zp * A.ncol + cg * 16, v);
+            if (ok && !(A.dbg & 1)) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                A.partial[(((int64_t)ks * A.nb + b) * (A.cout / 4) + n0 / 4 + cg * 4 + q) * S3 +
+                          ((int64_t)gz * S + gy) * S + gx] =
+                    make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+          }
+        }
+      } else if (A.epi == EPI_POOL) {
         const int px = gx >> 1, py = gy >> 1, pz = z0 >> 1;
         const bool writer = ((lane & 1) == 0) && ((ly & 1) == 0) && px < So && py < So && pz < So;
         for (int cg = 0; cg < A.ncol / 16; ++cg) {
@@ -414,6 +435,41 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
   }
 }
 
+// Fixed-order sum of the ksplit partials + bias + ReLU (+ 2x2x2 max pool) +
+// TF32 rounding into the output slot (deterministic: the split count depends
+// on the layer shape, never on the batch).
+__global__ void conv_split_reduce_kernel(const float4* __restrict__ part, int ksplit, int nb, int cq, int S,
+                                         const float* __restrict__ bias, int relu, int pool, float4* __restrict__ out,
+                                         int out_cq, int out_q0) {
+  const int So = pool ? S / 2 : S;
+  const int64_t S3 = (int64_t)S * S * S, So3 = (int64_t)So * So * So;
+  const int64_t total = (int64_t)nb * cq * So3;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t % So3;
+    const int64_t bq = t / So3;
+    const int q = bq % cq, b = bq / cq;
+    const int x = v % So, y = (v / So) % So, z = v / ((int64_t)So * So);
+    const float4 bb = bias ? make_float4(bias[4 * q], bias[4 * q + 1], bias[4 * q + 2], bias[4 * q + 3])
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 m = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    const int nw = pool ? 8 : 1;
+    for (int d = 0; d < nw; ++d) {
+      const int xx = pool ? 2 * x + (d & 1) : x, yy = pool ? 2 * y + ((d >> 1) & 1) : y,
+                zz = pool ? 2 * z + (d >> 2) : z;
+      const int64_t vi = ((int64_t)zz * S + yy) * S + xx;
+      float4 acc = part[((int64_t)b * cq + q) * S3 + vi];
+      for (int k = 1; k < ksplit; ++k) {
+        const float4 p = part[(((int64_t)k * nb + b) * cq + q) * S3 + vi];
+        acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+      }
+      m.x = fmaxf(m.x, acc.x); m.y = fmaxf(m.y, acc.y); m.z = fmaxf(m.z, acc.z); m.w = fmaxf(m.w, acc.w);
+    }
+    m.x += bb.x; m.y += bb.y; m.z += bb.z; m.w += bb.w;
+    if (relu) m = make_float4(fmaxf(m.x, 0.f), fmaxf(m.y, 0.f), fmaxf(m.z, 0.f), fmaxf(m.w, 0.f));
+    out[((int64_t)b * out_cq + out_q0 + q) * So3 + v] = tf32_round4(m);
+  }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -432,11 +488,38 @@ static EncodeTiledFn encode_fn() {
 
 }  // namespace tc
 
+// Split decisions for one layer shape (shared by the launch and the workspace plan).
+static void tc_split(int nb, int S, int cin, int cout, int& nsplit, int& ksplit) {
+  using namespace tc;
+  const int tiles_item = ceil_div(S, BX) * ceil_div(S, BY) * ceil_div(S, ZP);
+  const int nchunk = cin / 16;
+  nsplit = 1;
+  while (nb * tiles_item * nsplit < sm_count() && cout / (2 * nsplit) >= 32) nsplit *= 2;
+  // split-K only from the per-item shape so the FP32 summation order (hence
+  // the result) is independent of the batch size
+  int nsplit_item = 1;
+  while (tiles_item * nsplit_item < sm_count() && cout / (2 * nsplit_item) >= 32) nsplit_item *= 2;
+  ksplit = 1;
+  const int want = (sm_count() + tiles_item * nsplit_item - 1) / (tiles_item * nsplit_item);
+  if (tiles_item * nsplit_item * 2 <= sm_count())
+    for (int k = nchunk; k >= 2; --k)
+      if (nchunk % k == 0 && k <= want) {
+        ksplit = k;
+        break;
+      }
+}
+
+size_t tc_conv3_scratch_bytes(int nb, int S, int cin, int cout) {
+  int ns, ks;
+  tc_split(nb, S, cin, cout, ns, ks);
+  return ks > 1 ? (size_t)ks * nb * cout * S * S * S * sizeof(float) : 0;
+}
+
 int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int in_q0, const float* w,
              const float* bias, int relu, float4* out, int out_cq, int out_q0, int epi, const HeadArgs* head,
-             cudaStream_t st) {
+             void* scratch, size_t scratch_bytes, cudaStream_t st) {
   using namespace tc;
-  MDP_REQUIRE(cin % 8 == 0 && cin >= 8, "tc conv needs cin multiple of 8, got %d", cin);
+  MDP_REQUIRE(cin % 16 == 0 && cin >= 16, "tc conv needs cin multiple of 16, got %d", cin);
   MDP_REQUIRE(cout % 16 == 0 && cout >= 16 && cout <= 128, "tc conv needs cout in {16..128} step 16, got %d",
               cout);
   MDP_REQUIRE(epi == EPI_STORE || epi == EPI_POOL, "epilogue %d not supported by tc conv", epi);
@@ -453,12 +536,16 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   A.ty = ceil_div(S, BY);
   A.tz = ceil_div(S, ZP);
   const int spatial = nb * A.tx * A.ty * A.tz;
-  // small layers (few bricks): split the output channels over CTAs, down to
-  // 32 per CTA, until the grid covers the SMs
-  A.nsplit = 1;
-  while (spatial * A.nsplit < sm_count() && cout / (2 * A.nsplit) >= 32) A.nsplit *= 2;
+  // small layers (few bricks): split the output channels over CTAs (down to
+  // 32 per CTA) and, if still short of the SM count, the input chunks
+  tc_split(nb, S, cin, cout, A.nsplit, A.ksplit);
   A.ncol = cout / A.nsplit;
-  A.ntiles = spatial * A.nsplit;
+  A.cps = A.nchunk / A.ksplit;
+  A.ntiles = spatial * A.nsplit * A.ksplit;
+  A.partial = (float4*)scratch;
+  if (A.ksplit > 1)
+    MDP_REQUIRE(scratch && scratch_bytes >= tc_conv3_scratch_bytes(nb, S, cin, cout),
+                "split-K conv needs %zu bytes of scratch", tc_conv3_scratch_bytes(nb, S, cin, cout));
   A.in_cq = in_cq;
   A.in_q0 = in_q0;
   A.w = w;
@@ -475,7 +562,7 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   const size_t tap_bytes = (size_t)A.cqc * A.ncol * 16;
   A.resident = 0;
   int nbs = 0;
-  if (A.nchunk == 1 && (size_t)A.na * A.a_bytes + 27 * tap_bytes <= budget) {
+  if (A.cps == 1 && A.ksplit == 1 && (size_t)A.na * A.a_bytes + 27 * tap_bytes <= budget) {
     A.resident = 1;  // e.g. enc1b: the 27-tap filter fits next to the halo double buffer
     A.tps = 27;
     nbs = 1;
@@ -526,6 +613,16 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   int grid = A.ntiles < sm_count() ? A.ntiles : sm_count();
   conv3_tc_kernel<<<grid, 256, smem, st>>>(map, A);
   MDP_LAUNCH_CHECK("conv3_tc_kernel");
+  if (A.ksplit > 1) {
+    const int pool = epi == EPI_POOL;
+    const int So = pool ? S / 2 : S;
+    const int64_t total = (int64_t)nb * (cout / 4) * So * So * So;
+    int bx = ceil_div(total, 256);
+    bx = bx > 4 * sm_count() ? 4 * sm_count() : bx;
+    conv_split_reduce_kernel<<<bx, 256, 0, st>>>(A.partial, A.ksplit, nb, cout / 4, S, bias, relu, pool, out,
+                                                 out_cq, out_q0);
+    MDP_LAUNCH_CHECK("conv_split_reduce_kernel");
+  }
   return MDP_OK;
 }
 

@@ -42,9 +42,11 @@ def run_layer(path, x, k, bias, relu=True, pool=False, out_extra_quads=0):
     Bt = torch.as_tensor(bias.astype(np.float32), device="cuda") if bias is not None else None
     oq = cout // 4 + out_extra_quads
     Y = torch.full((b, oq, So, So, So, 4), float("nan"), dtype=torch.float32, device="cuda")
+    nscr = lib.mdp_conv3_scratch_bytes(b, S, cin, cout)
+    scr = torch.empty(max(nscr, 16), dtype=torch.uint8, device="cuda")
     _ext.check(lib.mdp_conv3_layer(path, b, S, cin, cout, X.data_ptr(), cin // 4, 0, W.data_ptr(),
                                    None if Bt is None else Bt.data_ptr(), int(relu), Y.data_ptr(), oq,
-                                   out_extra_quads, int(pool), _ext.stream()))
+                                   out_extra_quads, int(pool), scr.data_ptr(), nscr, _ext.stream()))
     y = Y.cpu().numpy()[:, out_extra_quads:]
     return from_c4(y, cout), Y.cpu().numpy()
 
