@@ -21,10 +21,10 @@ import oracle  # noqa: E402
 from oracle import problem as OP  # noqa: E402
 
 
-def cfg1_system():
+def cfg1_system(n_circle=8):
     g = OP.segment_graph([0.5, 0.5, 0.1], [0.5, 0.5, 0.9], 0.02)
     return OP.assemble_coupled_system(OP.StructuredGrid(17), g, OP.PhysicalParams(epsilon=0.02, beta=1.0),
-                                      n_circle=8, elems_per_edge=32, bc3d="dirichlet", f1d=1.0)
+                                      n_circle=n_circle, elems_per_edge=32, bc3d="dirichlet", f1d=1.0)
 
 
 def cfg2_system():
@@ -56,6 +56,11 @@ if __name__ == "__main__":
         print("cfg1 baseline semantics")
         u3, u1, rep = solve(cfg1_system(), 0, 300)
         np.savez_compressed(HERE / "solve_cfg1_baseline.npz", iters=rep.iterations, conv=rep.converged,
+                            hist=np.array(rep.residual_history), u3=u3, u1=u1)
+    if "cfg1c" in which:
+        print("cfg1 baseline semantics with the centreline restriction (n_circle=1)")
+        u3, u1, rep = solve(cfg1_system(1), 0, 300)
+        np.savez_compressed(HERE / "solve_cfg1_nc1.npz", iters=rep.iterations, conv=rep.converged,
                             hist=np.array(rep.residual_history), u3=u3, u1=u1)
     if "cfg2" in which:
         print("cfg2 baseline semantics, first 12 outer iterations")
