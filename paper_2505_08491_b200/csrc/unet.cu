@@ -147,43 +147,83 @@ __global__ void maxpool_kernel(const float4* __restrict__ in, int in_cq, int S, 
 }
 
 // Transposed conv k=2 s=2 (neural.py:215-246) + bias + ReLU, output size
-// 2*Sin+op; the op plane gets relu(bias) only.  w packed [cout/16][cin][8][16].
+// 2*Sin+op.  One block = one kernel tap (a,b,c) x 16 output channels over a
+// run of input voxels: the tap's weights (Cin x 16) sit in shared memory and
+// each input quad is read once, coalesced.  w packed [cout/16][cin][8][16].
 __global__ void __launch_bounds__(128) tconv_kernel(const float4* __restrict__ in, int in_cq, int cin,
                                                      int Sin, int op, const float* __restrict__ w,
                                                      const float* __restrict__ bias,
                                                      float4* __restrict__ out, int out_cq, int out_q0,
                                                      int round_tf32) {
-  extern __shared__ float wsh[];  // [cin][8][16]
-  const int g = blockIdx.y, b = blockIdx.z;
-  const float* wg = w + (int64_t)g * cin * 8 * 16;
-  for (int t = threadIdx.x; t < cin * 8 * 16; t += blockDim.x) wsh[t] = wg[t];
+  __shared__ float4 wsh[128 * 4];  // [cin][16] for this tap
+  const int tap = blockIdx.y & 7, g = blockIdx.y >> 3, b = blockIdx.z;
+  const float* wg = w + (size_t)g * cin * 8 * 16;
+  for (int t = threadIdx.x; t < cin * 4; t += blockDim.x) {
+    const int ci = t >> 2, c4 = t & 3;
+    const float* src = wg + ((size_t)ci * 8 + tap) * 16 + 4 * c4;
+    wsh[t] = make_float4(src[0], src[1], src[2], src[3]);
+  }
   __syncthreads();
   const int So = 2 * Sin + op;
   const int64_t nvo = (int64_t)So * So * So, nvi = (int64_t)Sin * Sin * Sin;
-  // persistent over output voxels: the weights are staged once per block
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvo; v += (int64_t)gridDim.x * blockDim.x) {
-  const int X = v % So, Y = (v / So) % So, Z = v / ((int64_t)So * So);
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= nvi) return;
+  const int x = v % Sin, y = (v / Sin) % Sin, z = v / ((int64_t)Sin * Sin);
   float acc[16];
 #pragma unroll
   for (int c = 0; c < 16; ++c) acc[c] = bias ? bias[g * 16 + c] : 0.f;
-  if (X < 2 * Sin && Y < 2 * Sin && Z < 2 * Sin) {
-    const int tap = ((Z & 1) * 2 + (Y & 1)) * 2 + (X & 1);
-    const int64_t vi = ((int64_t)(Z >> 1) * Sin + (Y >> 1)) * Sin + (X >> 1);
-    for (int q = 0; q < cin / 4; ++q) {
-      float4 a = __ldg(in + ((int64_t)b * in_cq + q) * nvi + vi);
-      const float* wt = wsh + ((4 * q) * 8 + tap) * 16;
+  for (int q = 0; q < cin / 4; ++q) {
+    const float4 a = __ldg(in + ((int64_t)b * in_cq + q) * nvi + v);
+    const float av[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
-        acc[c] += a.x * wt[c] + a.y * wt[8 * 16 + c] + a.z * wt[2 * 8 * 16 + c] + a.w * wt[3 * 8 * 16 + c];
+    for (int e = 0; e < 4; ++e) {
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const float4 wv = wsh[(4 * q + e) * 4 + c4];
+        acc[4 * c4] += av[e] * wv.x;
+        acc[4 * c4 + 1] += av[e] * wv.y;
+        acc[4 * c4 + 2] += av[e] * wv.z;
+        acc[4 * c4 + 3] += av[e] * wv.w;
+      }
     }
   }
+  const int X = 2 * x + (tap & 1), Y = 2 * y + ((tap >> 1) & 1), Z = 2 * z + (tap >> 2);
+  const int64_t o = ((int64_t)Z * So + Y) * So + X;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    float4 o = make_float4(fmaxf(acc[4 * q], 0.f), fmaxf(acc[4 * q + 1], 0.f), fmaxf(acc[4 * q + 2], 0.f),
+    float4 r = make_float4(fmaxf(acc[4 * q], 0.f), fmaxf(acc[4 * q + 1], 0.f), fmaxf(acc[4 * q + 2], 0.f),
                            fmaxf(acc[4 * q + 3], 0.f));
-    if (round_tf32) o = tf32_round4(o);
-    out[((int64_t)b * out_cq + out_q0 + g * 4 + q) * nvo + v] = o;
+    if (round_tf32) r = tf32_round4(r);
+    out[((int64_t)b * out_cq + out_q0 + g * 4 + q) * nvo + o] = r;
   }
+}
+
+// output-padding planes (index 2*Sin in any axis): relu(bias), no kernel mass
+__global__ void tconv_pad_kernel(int Sin, int cout, const float* __restrict__ bias, float4* __restrict__ out,
+                                 int out_cq, int out_q0, int nb, int round_tf32) {
+  const int So = 2 * Sin + 1, E = 2 * Sin;
+  const int64_t nvo = (int64_t)So * So * So;
+  const int64_t nplane = nvo - (int64_t)E * E * E;
+  const int64_t total = nplane * nb * (cout / 4);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t k = t % nplane;
+    const int64_t bq = t / nplane;
+    const int q = bq % (cout / 4), b = bq / (cout / 4);
+    // enumerate the voxels with max(X,Y,Z) == E: Z == E plane, then Y == E, then X == E
+    int X, Y, Z;
+    if (k < (int64_t)So * So) {
+      Z = E; Y = k / So; X = k % So;
+    } else if ((k -= (int64_t)So * So) < (int64_t)E * So) {
+      Z = k / So; Y = E; X = k % So;
+    } else {
+      k -= (int64_t)E * So;
+      Z = k / E; Y = k % E; X = E;
+    }
+    float4 r = bias ? make_float4(fmaxf(bias[4 * q], 0.f), fmaxf(bias[4 * q + 1], 0.f), fmaxf(bias[4 * q + 2], 0.f),
+                                  fmaxf(bias[4 * q + 3], 0.f))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (round_tf32) r = tf32_round4(r);
+    out[((int64_t)b * out_cq + out_q0 + q) * nvo + ((int64_t)Z * So + Y) * So + X] = r;
   }
 }
 
@@ -256,19 +296,19 @@ static int launch_pool(const float4* in, int in_cq, int S, int cq, float4* out, 
 static int launch_tconv(int nb, const float4* in, int in_cq, int cin, int cout, int Sin, int op, const float* w,
                         const float* bias, float4* out, int out_cq, int out_q0, int round_tf32,
                         cudaStream_t st) {
-  const int So = 2 * Sin + op;
-  const int smem = cin * 8 * 16 * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tconv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 8 * 16 * 4);
-    attr = true;
-  }
-  int bx = ceil_div((int64_t)So * So * So, 128);
-  const int cap = (2 * sm_count() + (cout / 16) * nb - 1) / ((cout / 16) * nb);
-  bx = bx > cap ? cap : bx;
-  dim3 grid(bx < 1 ? 1 : bx, cout / 16, nb);
-  tconv_kernel<<<grid, 128, smem, st>>>(in, in_cq, cin, Sin, op, w, bias, out, out_cq, out_q0, round_tf32);
+  MDP_REQUIRE(cin <= 128 && cin % 4 == 0 && cout % 16 == 0, "tconv needs cin<=128, cin%%4==0, cout%%16==0");
+  const int64_t nvi = (int64_t)Sin * Sin * Sin;
+  dim3 grid(ceil_div(nvi, 128), 8 * (cout / 16), nb);
+  tconv_kernel<<<grid, 128, 0, st>>>(in, in_cq, cin, Sin, op, w, bias, out, out_cq, out_q0, round_tf32);
   MDP_LAUNCH_CHECK("tconv_kernel");
+  if (op) {
+    const int So = 2 * Sin + 1;
+    const int64_t total = ((int64_t)So * So * So - 8 * nvi) * nb * (cout / 4);
+    int bx = ceil_div(total, 256);
+    bx = bx > 2 * sm_count() ? 2 * sm_count() : bx;
+    tconv_pad_kernel<<<bx, 256, 0, st>>>(Sin, cout, bias, out, out_cq, out_q0, nb, round_tf32);
+    MDP_LAUNCH_CHECK("tconv_pad_kernel");
+  }
   return MDP_OK;
 }
 
