@@ -42,145 +42,250 @@ __device__ __forceinline__ bool on_boundary(int i, int j, int k, int n) {
   return i == 0 || j == 0 || k == 0 || i == n - 1 || j == n - 1 || k == n - 1;
 }
 
-// One CTA: TX x TY columns of one system, z in [z0, z1).
-template <int TX, int TY>
-__global__ void __launch_bounds__(TX* TY) stencil_kernel(const mdp_problem P, const int32_t* sel,
-                                                         const double* __restrict__ x, int64_t ldx,
-                                                         double* __restrict__ y, int64_t ldy,
-                                                         int zchunk) {
-  __shared__ double xs[TY + 2][TX + 2];
-  __shared__ double sa[TY + 2][TX];
-  __shared__ double sb[TY + 2][TX];
-  const int n = P.n;
-  const int s = sys_of(sel, blockIdx.z);
-  const double* xp = x + (int64_t)s * ldx;
-  double* yp = y + (int64_t)s * ldy;
-  const int tiles_x = (n + TX - 1) / TX;
-  const int i0 = (blockIdx.x % tiles_x) * TX;
-  const int j0 = (blockIdx.x / tiles_x) * TY;
-  const int z0 = blockIdx.y * zchunk;
-  const int z1 = min(n, z0 + zchunk);
-  if (z0 >= n) return;
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
-  const int i = i0 + tx, j = j0 + ty;
-  const bool dir = P.bc3d != 0;
-  const Line1D c = make_line(P.h);
-  const double kO = P.k_omega, sO = P.sigma_omega;
-  const int64_t nn = (int64_t)n * n;
-
-  double Pm = 0.0, P0 = 0.0, Rm = 0.0, R0 = 0.0;
-  for (int kk = z0 - 1; kk <= z1; ++kk) {
-    double Pn = 0.0, Rn = 0.0;
-    const bool plane_ok = (kk >= 0 && kk < n);
-    if (plane_ok) {
-      for (int t = tid; t < (TY + 2) * (TX + 2); t += TX * TY) {
-        int ly = t / (TX + 2), lx = t - ly * (TX + 2);
-        int gi = i0 + lx - 1, gj = j0 + ly - 1;
-        double v = 0.0;
-        if (gi >= 0 && gi < n && gj >= 0 && gj < n) {
-          if (!(dir && on_boundary(gi, gj, kk, n))) v = __ldg(xp + kk * nn + (int64_t)gj * n + gi);
-        }
-        xs[ly][lx] = v;
-      }
-      __syncthreads();
-      for (int t = tid; t < (TY + 2) * TX; t += TX * TY) {
-        int ly = t / TX, lx = t - ly * TX;
-        int gi = i0 + lx;
-        double kd = kdiag(c, gi, n), md = mdiag(c, gi, n);
-        double a = c.ko * xs[ly][lx] + kd * xs[ly][lx + 1] + c.ko * xs[ly][lx + 2];
-        double b = c.mo * xs[ly][lx] + md * xs[ly][lx + 1] + c.mo * xs[ly][lx + 2];
-        sa[ly][lx] = a;
-        sb[ly][lx] = b;
-      }
-      __syncthreads();
-      double kd = kdiag(c, j, n), md = mdiag(c, j, n);
-      double c1 = c.mo * sa[ty][tx] + md * sa[ty + 1][tx] + c.mo * sa[ty + 2][tx];
-      double c2 = c.ko * sb[ty][tx] + kd * sb[ty + 1][tx] + c.ko * sb[ty + 2][tx];
-      double c3 = c.mo * sb[ty][tx] + md * sb[ty + 1][tx] + c.mo * sb[ty + 2][tx];
-      Pn = kO * (c1 + c2) + sO * c3;
-      Rn = kO * c3;
-    }
-    const int ko = kk - 1;  // output plane
-    if (ko >= z0 && ko < z1 && i < n && j < n) {
-      double kd = kdiag(c, ko, n), md = mdiag(c, ko, n);
-      double out = c.mo * Pm + md * P0 + c.mo * Pn + c.ko * Rm + kd * R0 + c.ko * Rn;
-      int64_t idx = ko * nn + (int64_t)j * n + i;
-      if (dir && on_boundary(i, j, ko, n)) out = xp[idx];
-      yp[idx] = out;
-    }
-    Pm = P0; P0 = Pn;
-    Rm = R0; R0 = Rn;
-  }
-}
-
 // s_q = W_q ((T x3)_q - (Psi D x1)_q): one warp per quadrature row, lanes
 // over the row's (point, corner) entries (8 for the centreline, up to 64
 // for the 8-point ring average), warp-shuffle reduction.  Entries on
 // eliminated (Dirichlet) cube nodes are dropped from T at build time.
+__device__ __forceinline__ void gather_rows(const mdp_problem& P, int s, int w0, int wstride,
+                                            const double* __restrict__ x3, const double* __restrict__ x1,
+                                            int64_t ld, double* __restrict__ s_out) {
+  const int lane = threadIdx.x & 31;
+  for (int q = P.q_start[s] + w0; q < P.q_start[s + 1]; q += wstride) {
+    double acc = 0.0;
+    if (x3) {
+      const double* xp = x3 + (int64_t)s * ld;
+      for (int k = P.t_ptr[q] + lane; k < P.t_ptr[q + 1]; k += 32) acc += P.t_val[k] * __ldg(xp + P.t_col[k]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      if (x1) {
+        const double* xp = x1 + (int64_t)s * ld;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          int col = P.psi_col[2 * q + e];
+          if (col >= 0) acc -= P.psi_val[2 * q + e] * xp[col];
+        }
+      }
+      s_out[q] = P.wq[q] * acc;
+    }
+  }
+}
+
+__device__ double g_zero_row[32];  // zero page: out-of-domain rows read from here
+
+// Warp-per-row-pair stencil: lane l owns column i = i0 - 1 + l (30 output
+// columns per warp, lanes 0 and 31 are the x halo), the warp owns rows j,
+// j+1 and marches z in [z0, z1).  Per plane each lane holds rows j-1..j+2
+// of its column in registers (two planes of loads in flight), takes its
+// x-neighbours by shuffle, forms the in-plane sum factorisation
+// P = kO (My Kx + Ky Mx) x + sO My Mx x, R = kO My Mx x for both rows
+// (the x products of the shared rows are reused) and carries P, R over
+// three planes: y = Mz P + Kz R.  No shared memory, no barriers; rows
+// outside the domain or on eliminated (Dirichlet) cube nodes read a zero
+// page through a pointer that does not advance.  Optional fused Jacobi
+// epilogue out = xin + omega (r - y) / diag(C) (coupling correction follows
+// in the pull).
+struct GatherArgs {  // optional Pi gather folded into the stencil launch (last y-slice)
+  const double* x3;
+  const double* x1;
+  double* s_out;
+};
+
+template <bool JAC, bool GATHER>
+__global__ void __launch_bounds__(128) stencil_kernel(const mdp_problem P, const int32_t* sel,
+                                                       const double* __restrict__ x, int64_t ldx,
+                                                       double* __restrict__ y, int64_t ldy, int zchunk,
+                                                       const double* __restrict__ jr, double omega,
+                                                       const GatherArgs G) {
+  constexpr int RY = 2, NR = RY + 2;
+  const int n = P.n;
+  const int s = sys_of(sel, blockIdx.z);
+  if (GATHER && blockIdx.y == gridDim.y - 1) {  // independent of the stencil: runs alongside it
+    gather_rows(P, s, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5), G.x3, G.x1,
+                ldx, G.s_out);
+    return;
+  }
+  const double* xp = x + (int64_t)s * ldx;
+  double* yp = y + (int64_t)s * ldy;
+  const int lane = threadIdx.x & 31;
+  const int tiles_x = (n + 29) / 30;
+  const int wrow = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int j = (wrow / tiles_x) * RY;
+  if (j >= n) return;
+  const int i = (wrow % tiles_x) * 30 - 1 + lane;
+  const int z0 = blockIdx.y * zchunk;
+  const int z1 = min(n, z0 + zchunk);
+  if (z0 >= n) return;
+  const bool dir = P.bc3d != 0;
+  const Line1D c = make_line(P.h);
+  const double kO = P.k_omega, sO = P.sigma_omega;
+  const int64_t nn = (int64_t)n * n;
+  const bool colok = i >= 0 && i < n && !(dir && (i == 0 || i == n - 1));
+  // per-row pointers at plane z0-1 and their per-plane step (0 for zero-page rows)
+  const double* ptr[NR];
+  int64_t step[NR];
+#pragma unroll
+  for (int a = 0; a < NR; ++a) {
+    const int jj = j - 1 + a;
+    const bool ok = colok && jj >= 0 && jj < n && !(dir && (jj == 0 || jj == n - 1));
+    ptr[a] = ok ? xp + (int64_t)(z0 - 1) * nn + (int64_t)jj * n + i : g_zero_row + lane;
+    step[a] = ok ? nn : 0;
+  }
+  // plane kk contributes values iff it lies inside and is not an eliminated face
+  auto plane_ok = [&](int kk) { return kk >= 0 && kk < n && !(dir && (kk == 0 || kk == n - 1)); };
+  auto load = [&](int kk, double* v) {
+    const bool pok = plane_ok(kk);
+#pragma unroll
+    for (int a = 0; a < NR; ++a) {
+      v[a] = pok ? __ldg(ptr[a]) : 0.0;
+      ptr[a] += step[a];
+    }
+  };
+  const bool out_lane = lane >= 1 && lane <= 30 && i < n;
+  const int ic = i < 0 ? 0 : (i >= n ? n - 1 : i);
+  const double kdx = kdiag(c, ic, n), mdx = mdiag(c, ic, n);
+  double kdy[RY], mdy[RY];
+  bool rok[RY], colb[RY];
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+    const int jr_ = j + r < n ? j + r : n - 1;
+    kdy[r] = kdiag(c, jr_, n);
+    mdy[r] = mdiag(c, jr_, n);
+    rok[r] = out_lane && j + r < n;
+    colb[r] = dir && (i == 0 || i == n - 1 || j + r == 0 || j + r == n - 1);
+  }
+  double* yrow = yp + (int64_t)z0 * nn + (int64_t)j * n + i;  // output (z0, j, i)
+  const double* xrow = xp + (int64_t)z0 * nn + (int64_t)j * n + i;
+  int64_t goff = (int64_t)s * ldy + (int64_t)z0 * nn + (int64_t)j * n + i;
+  double cur[NR], nx1[NR], nx2[NR];
+  load(z0 - 1, cur);
+  load(z0, nx1);
+  double Pm[RY], P0[RY], Rm[RY], R0[RY];
+#pragma unroll
+  for (int r = 0; r < RY; ++r) Pm[r] = P0[r] = Rm[r] = R0[r] = 0.0;
+  for (int kk = z0 - 1; kk <= z1; ++kk) {
+    if (kk + 2 <= z1) load(kk + 2, nx2);
+    double kx[NR], mx[NR];
+#pragma unroll
+    for (int a = 0; a < NR; ++a) {
+      const double lr = __shfl_up_sync(0xffffffffu, cur[a], 1) + __shfl_down_sync(0xffffffffu, cur[a], 1);
+      kx[a] = c.ko * lr + kdx * cur[a];
+      mx[a] = c.mo * lr + mdx * cur[a];
+    }
+    const int ko = kk - 1;
+    const bool emit = ko >= z0;
+    const double kd = kdiag(c, ko < 0 ? 0 : ko, n), md = mdiag(c, ko < 0 ? 0 : ko, n);
+    const bool planeb = dir && (ko == 0 || ko == n - 1);
+#pragma unroll
+    for (int r = 0; r < RY; ++r) {
+      const double msum = mx[r] + mx[r + 2];
+      const double c1 = c.mo * (kx[r] + kx[r + 2]) + mdy[r] * kx[r + 1];
+      const double c2 = c.ko * msum + kdy[r] * mx[r + 1];
+      const double c3 = c.mo * msum + mdy[r] * mx[r + 1];
+      const double Pn = kO * (c1 + c2) + sO * c3;
+      const double Rn = kO * c3;
+      if (emit && rok[r]) {
+        double out = c.mo * (Pm[r] + Pn) + md * P0[r] + c.ko * (Rm[r] + Rn) + kd * R0[r];
+        if (colb[r] || planeb) out = xrow[r * n];
+        if (JAC) out = xrow[r * n] + (omega * (jr[goff + r * n] - out)) / P.diag_c[goff + r * n];
+        yrow[r * n] = out;
+      }
+      Pm[r] = P0[r]; P0[r] = Pn;
+      Rm[r] = R0[r]; R0[r] = Rn;
+    }
+    if (emit) {
+      yrow += nn;
+      xrow += nn;
+      goff += nn;
+    }
+#pragma unroll
+    for (int a = 0; a < NR; ++a) {
+      cur[a] = nx1[a];
+      nx1[a] = nx2[a];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) pi_gather_kernel(const mdp_problem P, const int32_t* sel,
                                                          const double* __restrict__ x3,
                                                          const double* __restrict__ x1, int64_t ld,
                                                          double* __restrict__ s_out) {
   const int s = sys_of(sel, blockIdx.y);
-  const int lane = threadIdx.x & 31;
-  const int q = P.q_start[s] + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (q >= P.q_start[s + 1]) return;
-  double acc = 0.0;
-  if (x3) {
-    const double* xp = x3 + (int64_t)s * ld;
-    for (int k = P.t_ptr[q] + lane; k < P.t_ptr[q + 1]; k += 32) acc += P.t_val[k] * __ldg(xp + P.t_col[k]);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) {
-    if (x1) {
-      const double* xp = x1 + (int64_t)s * ld;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        int col = P.psi_col[2 * q + e];
-        if (col >= 0) acc -= P.psi_val[2 * q + e] * xp[col];
-      }
-    }
-    s_out[q] = P.wq[q] * acc;
-  }
+  gather_rows(P, s, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5), x3, x1, ld,
+              s_out);
 }
 
-// y3[u] += alpha w_s (T^T s)[u]: 8 lanes per touched free node, no atomics
-__global__ void __launch_bounds__(256) pi_pull_kernel(const mdp_problem P, const int32_t* sel,
-                                                       const double* __restrict__ sv, double alpha,
-                                                       double* __restrict__ y3, int64_t ld) {
-  const int s = sys_of(sel, blockIdx.y);
+// y3[u] += alpha w_s (T^T s)[u] (/ div[u] when div is given: the Jacobi
+// coupling correction): 8 lanes per touched free node, no atomics
+__device__ __forceinline__ void pull_rows(const mdp_problem& P, int s, int g0, int gstride,
+                                          const double* __restrict__ sv, double alpha, double* __restrict__ y3,
+                                          int64_t ld, const double* __restrict__ div) {
   const int sub = threadIdx.x & 7;
-  const int u = P.u_start[s] + blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3);
-  const bool live = u < P.u_start[s + 1];
-  double acc = 0.0;
-  if (live)
-    for (int k = P.u_ptr[u] + sub; k < P.u_ptr[u + 1]; k += 8) acc += P.u_val[k] * sv[P.u_q[k]];
+  const int ucount = P.u_start[s + 1] - P.u_start[s];
+  // the 8-lane groups of a warp iterate together (shuffles need all lanes)
+  const int gfirst = g0 - ((threadIdx.x & 31) >> 3);
+  for (int it = 0; gfirst + it * gstride < ucount; ++it) {
+    const int base = g0 + it * gstride;
+    const int u = P.u_start[s] + base;
+    const bool live = base < ucount;
+    double acc = 0.0;
+    if (live)
+      for (int k = P.u_ptr[u] + sub; k < P.u_ptr[u + 1]; k += 8) acc += P.u_val[k] * sv[P.u_q[k]];
 #pragma unroll
-  for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (live && sub == 0) y3[(int64_t)s * ld + P.u_node[u]] += alpha * P.wc[s] * acc;
+    for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (live && sub == 0) {
+      const int64_t g = (int64_t)s * ld + P.u_node[u];
+      if (div)
+        y3[g] -= (-alpha * (P.wc[s] * acc)) / div[g];
+      else
+        y3[g] += alpha * P.wc[s] * acc;
+    }
+  }
 }
 
 // y1 = K11 x1 - w D Psi^T s: 4 lanes per 1D row
-__global__ void __launch_bounds__(256) oned_kernel(const mdp_problem P, const int32_t* sel,
-                                                    const double* __restrict__ x1, const double* __restrict__ sv,
-                                                    double* __restrict__ y1, int64_t ld) {
-  const int s = sys_of(sel, blockIdx.y);
+__device__ __forceinline__ void oned_rows(const mdp_problem& P, int s, int g0, int gstride,
+                                          const double* __restrict__ x1, const double* __restrict__ sv,
+                                          double* __restrict__ y1, int64_t ld) {
   const int sub = threadIdx.x & 3;
-  const int r = P.r1_start[s] + blockIdx.x * (blockDim.x >> 2) + (threadIdx.x >> 2);
-  const bool live = r < P.r1_start[s + 1];
+  const int rcount = P.r1_start[s + 1] - P.r1_start[s];
   const double* xp = x1 + (int64_t)s * ld;
-  double a = 0.0, b = 0.0;
-  if (live) {
-    for (int k = P.k_ptr[r] + sub; k < P.k_ptr[r + 1]; k += 4) a += P.k_val[k] * xp[P.k_col[k]];
-    for (int k = P.p_ptr[r] + sub; k < P.p_ptr[r + 1]; k += 4) b += P.p_val[k] * sv[P.p_q[k]];
-  }
+  const int gfirst = g0 - ((threadIdx.x & 31) >> 2);
+  for (int it = 0; gfirst + it * gstride < rcount; ++it) {
+    const int base = g0 + it * gstride;
+    const int r = P.r1_start[s] + base;
+    const bool live = base < rcount;
+    double a = 0.0, b = 0.0;
+    if (live) {
+      for (int k = P.k_ptr[r] + sub; k < P.k_ptr[r + 1]; k += 4) a += P.k_val[k] * xp[P.k_col[k]];
+      for (int k = P.p_ptr[r] + sub; k < P.p_ptr[r + 1]; k += 4) b += P.p_val[k] * sv[P.p_q[k]];
+    }
 #pragma unroll
-  for (int o = 2; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
+    for (int o = 2; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (live && sub == 0) y1[(int64_t)s * ld + base] = a - P.wc[s] * b;
   }
-  if (live && sub == 0) y1[(int64_t)s * ld + (r - P.r1_start[s])] = a - P.wc[s] * b;
+}
+
+// Second phase of the coupled / reduced SpMV and of the Jacobi sweep in one
+// launch: blocks [0, bpull) pull T^T s into y3, the rest form the 1D rows.
+__global__ void __launch_bounds__(256) coupling_phase2_kernel(const mdp_problem P, const int32_t* sel, int bpull,
+                                                               const double* __restrict__ sv, double alpha,
+                                                               double* __restrict__ y3, int64_t ld,
+                                                               const double* __restrict__ div,
+                                                               const double* __restrict__ x1,
+                                                               double* __restrict__ y1) {
+  const int s = sys_of(sel, blockIdx.y);
+  if ((int)blockIdx.x < bpull) {
+    pull_rows(P, s, blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3), bpull * (blockDim.x >> 3), sv, alpha, y3,
+              ld, div);
+  } else if (y1) {
+    const int b = blockIdx.x - bpull, nb = gridDim.x - bpull;
+    oned_rows(P, s, b * (blockDim.x >> 2) + (threadIdx.x >> 2), nb * (blockDim.x >> 2), x1, sv, y1, ld);
+  }
 }
 
 // x_out = x + (omega (r - Cx)) / diag  (Cx in tmp); x == NULL means x = 0 and Cx = 0
@@ -234,17 +339,35 @@ __global__ void __launch_bounds__(256) distance_kernel(int n, const double* __re
 }
 
 static int launch_stencil(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* x,
-                          int64_t ldx, double* y, int64_t ldy, cudaStream_t st) {
+                          int64_t ldx, double* y, int64_t ldy, cudaStream_t st, const double* jr = nullptr,
+                          double omega = 0.0, const GatherArgs* g = nullptr) {
   const int n = p->n;
-  constexpr int TX = 32, TY = 8;
-  int tiles = ceil_div(n, TX) * ceil_div(n, TY);
-  int want = 6 * sm_count();
-  int zch = ceil_div(want, (int64_t)tiles * nsel);
-  zch = zch < 1 ? 1 : (zch > n ? n : zch);
+  const int64_t warps = (int64_t)ceil_div(n, 30) * ceil_div(n, 2);  // (x-tile, row pair) per plane
+  int bx = ceil_div(warps, 4);
+  // z-chunks: enough warps to fill the machine; chunks of >= 16 planes when the
+  // problem is large, down to 4 planes when it is latency-bound anyway
+  int64_t want = (int64_t)48 * 4 * sm_count();
+  int zch = ceil_div(want, warps * nsel);
+  const int zmin_len = warps * nsel * (n / 16) >= want ? 16 : 4;
+  const int zmax = n / zmin_len > 1 ? n / zmin_len : 1;
+  zch = zch < 1 ? 1 : (zch > zmax ? zmax : zch);
   int zchunk = ceil_div(n, zch);
   zch = ceil_div(n, zchunk);
-  dim3 grid(tiles, zch, nsel), block(TX, TY);
-  stencil_kernel<TX, TY><<<grid, block, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk);
+  const bool gat = g != nullptr && p->qmax > 0;
+  if (gat) bx = bx > ceil_div(p->qmax, 4) ? bx : ceil_div(p->qmax, 4);  // one warp per Pi row in the gather slice
+  dim3 grid(bx, zch + (gat ? 1 : 0), nsel);
+  GatherArgs G = gat ? *g : GatherArgs{nullptr, nullptr, nullptr};
+  if (jr) {
+    if (gat)
+      stencil_kernel<true, true><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
+    else
+      stencil_kernel<true, false><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
+  } else {
+    if (gat)
+      stencil_kernel<false, true><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
+    else
+      stencil_kernel<false, false><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
+  }
   MDP_LAUNCH_CHECK("stencil_kernel");
   return MDP_OK;
 }
@@ -258,21 +381,16 @@ static int launch_gather(const mdp_problem* p, int32_t nsel, const int32_t* sel,
   return MDP_OK;
 }
 
-static int launch_pull(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* s,
-                       double alpha, double* y3, int64_t ld, cudaStream_t st) {
-  if (p->umax <= 0) return MDP_OK;
-  dim3 grid(ceil_div(p->umax, 32), nsel);
-  pi_pull_kernel<<<grid, 256, 0, st>>>(*p, sel, s, alpha, y3, ld);
-  MDP_LAUNCH_CHECK("pi_pull_kernel");
-  return MDP_OK;
-}
-
-static int launch_oned(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* x1,
-                       const double* s, double* y1, int64_t ld, cudaStream_t st) {
-  if (p->r1max <= 0) return MDP_OK;
-  dim3 grid(ceil_div(p->r1max, 64), nsel);
-  oned_kernel<<<grid, 256, 0, st>>>(*p, sel, x1, s, y1, ld);
-  MDP_LAUNCH_CHECK("oned_kernel");
+// pull T^T s into y3 (and, with y1, the 1D rows) in one launch
+static int launch_phase2(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* s, double alpha,
+                         double* y3, int64_t ld, cudaStream_t st, const double* div, const double* x1,
+                         double* y1) {
+  const int bpull = p->umax > 0 ? ceil_div(p->umax, 32) : 0;
+  const int boned = (y1 && p->r1max > 0) ? ceil_div(p->r1max, 64) : 0;
+  if (bpull + boned == 0) return MDP_OK;
+  dim3 grid(bpull + boned, nsel);
+  coupling_phase2_kernel<<<grid, 256, 0, st>>>(*p, sel, bpull, s, alpha, y3, ld, div, x1, y1);
+  MDP_LAUNCH_CHECK("coupling_phase2_kernel");
   return MDP_OK;
 }
 
@@ -317,7 +435,7 @@ extern "C" int mdp_pi_scatter(const mdp_problem* p, int32_t nsel, const int32_t*
                               void* stream) {
   if (int rc = validate(p, nsel)) return rc;
   if (nsel == 0) return MDP_OK;
-  return launch_pull(p, nsel, sel, s, alpha, y3, ld, (cudaStream_t)stream);
+  return launch_phase2(p, nsel, sel, s, alpha, y3, ld, (cudaStream_t)stream, nullptr, nullptr, nullptr);
 }
 
 extern "C" int mdp_coupled_spmv(const mdp_problem* p, int32_t nsel, const int32_t* sel,
@@ -326,11 +444,12 @@ extern "C" int mdp_coupled_spmv(const mdp_problem* p, int32_t nsel, const int32_
   if (nsel == 0) return MDP_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n3 = (int64_t)p->n * p->n * p->n;
+  // launch 1: stencil y3 = K00 x3 with the Pi gather s = W (T x3 - Psi D x1) alongside;
+  // launch 2: y3 += w T^T s and y1 = K11 x1 - w D Psi^T s
+  GatherArgs g{x, x + n3, s_work};
   int rc;
-  if ((rc = launch_gather(p, nsel, sel, x, x + n3, p->ld, s_work, st))) return rc;
-  if ((rc = launch_stencil(p, nsel, sel, x, p->ld, y, p->ld, st))) return rc;
-  if ((rc = launch_pull(p, nsel, sel, s_work, 1.0, y, p->ld, st))) return rc;
-  return launch_oned(p, nsel, sel, x + n3, s_work, y + n3, p->ld, st);
+  if ((rc = launch_stencil(p, nsel, sel, x, p->ld, y, p->ld, st, nullptr, 0.0, &g))) return rc;
+  return launch_phase2(p, nsel, sel, s_work, 1.0, y, p->ld, st, nullptr, x + n3, y + n3);
 }
 
 extern "C" int mdp_reduced_spmv(const mdp_problem* p, int32_t nsel, const int32_t* sel,
@@ -338,10 +457,10 @@ extern "C" int mdp_reduced_spmv(const mdp_problem* p, int32_t nsel, const int32_
   if (int rc = validate(p, nsel)) return rc;
   if (nsel == 0) return MDP_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  GatherArgs g{x3, nullptr, s_work};
   int rc;
-  if ((rc = launch_gather(p, nsel, sel, x3, nullptr, p->ld, s_work, st))) return rc;
-  if ((rc = launch_stencil(p, nsel, sel, x3, p->ld, y3, p->ld, st))) return rc;
-  return launch_pull(p, nsel, sel, s_work, 1.0, y3, p->ld, st);
+  if ((rc = launch_stencil(p, nsel, sel, x3, p->ld, y3, p->ld, st, nullptr, 0.0, &g))) return rc;
+  return launch_phase2(p, nsel, sel, s_work, 1.0, y3, p->ld, st, nullptr, nullptr, nullptr);
 }
 
 extern "C" int mdp_jacobi_sweep(const mdp_problem* p, int32_t nsel, const int32_t* sel,
@@ -352,9 +471,14 @@ extern "C" int mdp_jacobi_sweep(const mdp_problem* p, int32_t nsel, const int32_
   if (nsel == 0) return MDP_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (x) {
-    int rc = mdp_reduced_spmv(p, nsel, sel, x, tmp, s_work, stream);
-    if (rc) return rc;
+    // fused sweep: s = W T x; out = x + omega (r - K00 x) / d in the stencil
+    // epilogue; then out -= omega w (T^T s) / d at the touched nodes
+    GatherArgs g{x, nullptr, s_work};
+    int rc;
+    if ((rc = launch_stencil(p, nsel, sel, x, p->ld, x_out, p->ld, st, r, omega, &g))) return rc;
+    return launch_phase2(p, nsel, sel, s_work, -omega, x_out, p->ld, st, p->diag_c, nullptr, nullptr);
   }
+  (void)tmp;
   const int64_t n3 = (int64_t)p->n * p->n * p->n;
   int bx = ceil_div(n3, 256);
   bx = bx > 4096 ? 4096 : bx;

@@ -1,0 +1,145 @@
+"""BASELINE config 5: operator microbenchmark sweep (no solve).
+
+Grids n in {33, 65, 129, 193} x batch {1, 8, 64} of seeded 32-segment trees.
+Timed separately (CUDA events, warm, L2 flushed before every timed rep):
+coupled block SpMV, Pi gather, Pi^T scatter (pull), 30-vector Arnoldi
+orthogonalisation, and the CNN preconditioner forward.  Algorithmic bytes /
+FLOPs per SURVEY.md section 8d; peaks from MEASURED_PEAKS.json (HBM) and a
+cuBLAS TF32 GEMM measured in the same run.
+
+    python tools/bench_ops.py [--sizes 33,65,129,193] [--batches 1,8,64] [--out f.json]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2505_08491_b200 import _ext, configs, neural  # noqa: E402
+
+
+def timed(fn, reps, flush):
+    ts = []
+    for _ in range(reps):
+        bench.flush_l2(flush)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        e.synchronize()
+        ts.append(s.elapsed_time(e))
+    ts.sort()
+    return ts[len(ts) // 2]  # median ms
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes", default="33,65,129,193")
+    ap.add_argument("--batches", default="1,8,64")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--mem-gb", type=float, default=120.0)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    lib = _ext.lib()
+    pk = bench.peaks()
+    tf32 = bench.measure_tf32_peak()
+    flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device="cuda")
+    from paper_2505_08491_b200.assembly import DeviceProblem
+    from paper_2505_08491_b200.operators import CoupledOperator, CouplingOps
+    rows = []
+    net = neural.DeviceUNet(neural.perturbed_params(4))
+    for n in [int(x) for x in a.sizes.split(",")]:
+        for nb in [int(x) for x in a.batches.split(",")]:
+            n3 = n ** 3
+            # memory guard: vectors + CNN workspace
+            est = nb * (n3 * 8 * 40 + lib.mdp_unet_workspace_bytes(n, 1, 0))
+            if est > a.mem_gb * 1e9:
+                rows.append({"n": n, "batch": nb, "skipped": f"needs ~{est / 1e9:.0f} GB"})
+                continue
+            t0 = time.time()
+            systems = configs.cfg5_systems(n, nb)
+            prob = DeviceProblem(systems)
+            A = CoupledOperator(prob)
+            ops = CouplingOps(prob)
+            X = prob.zeros().normal_()
+            Y = prob.zeros()
+            N = [n3 + int(x) for x in prob.n1]
+            Q = prob.Qtot
+            U = int(prob._t["u_start"][-1].item())
+            r = {"n": n, "batch": nb, "Q_total": Q, "setup_s": round(time.time() - t0, 2)}
+            ms = timed(lambda: A.matvec(X, Y), a.reps, flush)
+            byt = sum(16 * x for x in N) + 40 * Q
+            r["spmv"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9, "frac_hbm": byt / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                         "bytes": byt}
+            S = torch.zeros(max(Q, 1), dtype=torch.float64, device="cuda")
+            ms = timed(lambda: ops.gather(X, None, S), a.reps, flush)
+            byt = 112 * Q
+            r["pi_gather"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9, "bytes": byt}
+            ms = timed(lambda: ops.scatter(S, 1.0, Y), a.reps, flush)
+            byt = 48 * Q + 16 * U
+            r["pi_scatter"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9, "bytes": byt}
+            # Arnoldi: 30 basis vectors (k = 30), orthogonalise w against all of them
+            k = 30
+            nmax = max(N)
+            if nb * (k + 2) * prob.ld * 8 < 60e9:
+                V = torch.randn((nb, k + 1, prob.ld), dtype=torch.float64, device="cuda")
+                W = torch.randn((nb, prob.ld), dtype=torch.float64, device="cuda")
+                H = torch.zeros((nb, k + 2), dtype=torch.float64, device="cuda")
+                nv = torch.full((nb,), k, dtype=torch.int32, device="cuda")
+                work = torch.zeros(lib.mdp_arnoldi_work_bytes(nb, k, nmax) // 8 + 1, dtype=torch.float64,
+                                   device="cuda")
+
+                def arn():
+                    _ext.check(lib.mdp_arnoldi(nb, None, V.data_ptr(), (k + 1) * prob.ld, prob.ld, nv.data_ptr(), k,
+                                               W.data_ptr(), prob.ld, nmax, H.data_ptr(), None, 0, work.data_ptr(),
+                                               _ext.stream()))
+                ms = timed(arn, a.reps, flush)
+                byt = (2 * k + 3) * nmax * 8 * nb
+                r["arnoldi30"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9,
+                                  "frac_hbm": byt / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], "bytes": byt,
+                                  "note": "CGS2: V read 3x; bytes = survey formula (2k+3) N 8"}
+                del V, W
+            # CNN forward (pack -> U-Net -> rescale), batch nb
+            D = torch.rand((nb, n3), dtype=torch.float64, device="cuda")
+            R = X
+            rn = torch.ones(nb, dtype=torch.float64, device="cuda")
+            Z = prob.zeros()
+            ms = timed(lambda: net.apply(n, R, prob.ld, rn, D, n3, Z, prob.ld, nb=nb), max(3, a.reps // 2), flush)
+            fl = nb * neural_flops(n)
+            r["cnn_forward"] = {"ms": ms, "TFLOPs": fl / (ms * 1e-3) / 1e12, "frac_tf32": fl / (ms * 1e-3) / 1e12 / tf32,
+                                "flops": fl}
+            rows.append(r)
+            print(json.dumps(r), flush=True)
+            del prob, A, ops, X, Y, S, D, Z, R
+            torch.cuda.empty_cache()
+    out = {"peaks": pk, "tf32_tflops_measured": tf32, "rows": rows}
+    if a.out:
+        Path(a.out).write_text(json.dumps(out, indent=1))
+
+
+def neural_flops(n: int) -> float:
+    m, q = n // 2, n // 4
+    f = 0.0
+    for name, op, cin, cout, ks, _ in neural.ARCHITECTURE:
+        if op == "tconv":
+            out = m ** 3 if name == "up2" else n ** 3  # survey convention: 2 * voxels_out * Cin * Cout
+            f += 2.0 * out * cin * cout
+        else:
+            vox = {"enc3": m ** 3, "dec2": m ** 3, "bottleneck": q ** 3}.get(name, n ** 3)
+            f += 2.0 * vox * cin * cout * ks ** 3
+    return f
+
+
+if __name__ == "__main__":
+    main()

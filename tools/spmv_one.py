@@ -1,0 +1,15 @@
+"""Coupled SpMV on cfg5-style systems (for ncu)."""
+import sys
+sys.path.insert(0, ".")
+import torch
+from paper_2505_08491_b200 import configs
+from paper_2505_08491_b200.assembly import DeviceProblem
+from paper_2505_08491_b200.operators import ReducedOperator
+n, nb, reps = (int(a) for a in sys.argv[1:4])
+p = DeviceProblem(configs.cfg5_systems(n, nb))
+C = ReducedOperator(p)
+X = p.zeros().normal_(); Y = p.zeros()
+for _ in range(reps):
+    C.matvec(X, Y)
+torch.cuda.synchronize()
+print("ok")
