@@ -205,7 +205,7 @@ def run_reference(args):
         if step >= args.warmup:
             times.append(dt)
     per_iter = statistics.median(times) / sample
-    full = EXPECTED_ITERS.get(args.workload) or wl.maxit
+    full = args.maxit or EXPECTED_ITERS.get(args.workload) or wl.maxit
     value = 1.0 / (per_iter * full) * len(wl.systems)
     cores = len(os.sched_getaffinity(0))
     line = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": args.gpus, "steps": args.steps,
@@ -238,6 +238,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2505_08491_b200 import _ext, configs, harness, neural
+    from paper_2505_08491_b200.replicas import aggregate_throughput
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -281,13 +282,8 @@ def run_ours(args):
             e.synchronize()
             ms_steps.append(s.elapsed_time(e))
     launches = lib.mdp_launch_count() + solver.outer.replayed_kernels - l0
-    t_local = sum(ms_steps)
-    t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_max = float(t.item())
-    nsolve = len(wl.systems) * args.steps * world
-    value = nsolve / (t_max * 1e-3)
+    # whole job: all ranks' solves / the slowest rank's device time (replicas, no data-path collective)
+    value, t_max, _ = aggregate_throughput(sum(ms_steps), len(wl.systems) * args.steps, device="cuda")
 
     # -- preconditioner applies/s (smoothed CNN apply, batched over the workload systems)
     P = solver.inner
