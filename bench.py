@@ -107,6 +107,41 @@ def flush_l2(buf):
     buf.add_(1.0)  # 256 MiB write > 126 MB L2
 
 
+def device_ms(fn, reps=20, flush=None, hide_us=None):
+    """Median device time (ms) of fn() over reps, CUDA events on the current stream.
+
+    A GPU sleep queued ahead of each timed call keeps the device busy while the
+    host enqueues fn (ctypes marshalling takes longer than a small kernel), so
+    the events bracket device work only.  flush: L2-flush buffer written before
+    every rep (cold-cache timing), else back-to-back warm reps.
+    """
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    cycles = int((hide_us or 400) * 2000)  # ~2 GHz
+    ts = []
+    if flush is None:
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(cycles * reps)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        e.synchronize()
+        return s.elapsed_time(e) / reps
+    for _ in range(reps):
+        flush_l2(flush)
+        torch.cuda._sleep(cycles)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        e.synchronize()
+        ts.append(s.elapsed_time(e))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
 def measure_tf32_peak():
     """cuBLAS TF32 GEMM 8192^3, best of 5 (the tensor-core denominator for kind::tf32)."""
     import torch
@@ -151,18 +186,72 @@ def conv_layer_times(n, reps=20):
         def run():
             _ext.check(lib.mdp_conv3_layer(0, 1, S, cin, cout, X.data_ptr(), cin // 4, 0, W.data_ptr(), None, 1,
                                            Y.data_ptr(), cout // 4, 0, pool, scr.data_ptr(), scr.numel(), st))
-        run()
-        torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        for _ in range(reps):
-            run()
-        e.record()
-        e.synchronize()
-        ms = s.elapsed_time(e) / reps
+        ms = device_ms(run, reps)
         flops = 2.0 * S ** 3 * cin * cout * 27
         out[name] = {"ms": ms, "flops": flops, "tflops": flops / (ms * 1e-3) / 1e12, "S": S}
     return out
+
+
+def target_128(tf32_peak, hbm_peak):
+    """The north star's target configuration (BASELINE cfg4, 128^3 cells = 129^3
+    nodes): conv layers vs the TF32 tensor peak, the CNN forward, and the
+    coupled SpMV (L2 flushed before every rep) vs the HBM peak."""
+    import torch
+    from paper_2505_08491_b200 import configs, neural
+    from paper_2505_08491_b200.operators import CoupledOperator
+    from paper_2505_08491_b200.assembly import DeviceProblem
+    n = 129
+    layers = conv_layer_times(n, reps=5)
+    dom = max(layers, key=lambda k: layers[k]["ms"])
+    stack_ms = sum(v["ms"] for v in layers.values())
+    stack_fl = sum(v["flops"] for v in layers.values())
+    net = neural.DeviceUNet(neural.perturbed_params(3))
+    R = torch.randn((1, n ** 3), dtype=torch.float64, device="cuda")
+    D = torch.rand((1, n ** 3), dtype=torch.float64, device="cuda")
+    rn = torch.ones(1, dtype=torch.float64, device="cuda")
+    Z = torch.empty_like(R)
+    fwd_ms = device_ms(lambda: net.apply(n, R, n ** 3, rn, D, n ** 3, Z, n ** 3, nb=1), 5)
+    fwd_fl = neural_forward_flops(n)
+    del R, D, Z
+    wl = configs.cfg4()
+    prob = DeviceProblem(wl.systems)
+    A = CoupledOperator(prob)
+    X = prob.zeros().normal_()
+    Y = prob.zeros()
+    flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device="cuda")
+    sp_ms = device_ms(lambda: A.matvec(X, Y), 10, flush=flush)
+    sp_bytes = sum(16 * (prob.n3 + int(n1)) for n1 in prob.n1) + 40 * prob.Qtot
+    out = {
+        "config": "cfg4: 128^3 cells (129^3 nodes), 64-segment tree, 32 elements/segment",
+        "conv_dominant": {"bound": "tensor", "kernel": f"conv3_tc_kernel ({dom})", "ms": layers[dom]["ms"],
+                          "achieved": layers[dom]["tflops"], "peak": tf32_peak, "unit": "TFLOP/s",
+                          "frac": layers[dom]["tflops"] / tf32_peak},
+        "conv_stack": {"ms": stack_ms, "achieved": stack_fl / (stack_ms * 1e-3) / 1e12,
+                       "frac": stack_fl / (stack_ms * 1e-3) / 1e12 / tf32_peak, "unit": "TFLOP/s",
+                       "layers": {k: round(v["tflops"], 1) for k, v in layers.items()}},
+        "cnn_forward": {"ms": fwd_ms, "achieved": fwd_fl / (fwd_ms * 1e-3) / 1e12,
+                        "frac": fwd_fl / (fwd_ms * 1e-3) / 1e12 / tf32_peak, "unit": "TFLOP/s",
+                        "note": "pack + 9 conv/tconv layers + heads; flops per SURVEY.md 8d"},
+        "spmv": {"bound": "hbm", "ms": sp_ms, "bytes": sp_bytes, "achieved": sp_bytes / (sp_ms * 1e-3) / 1e9,
+                 "peak": hbm_peak, "unit": "GB/s", "frac": sp_bytes / (sp_ms * 1e-3) / 1e9 / hbm_peak,
+                 "note": "L2 flushed before every rep"},
+    }
+    del prob, A, X, Y, flush, net
+    torch.cuda.empty_cache()
+    return out
+
+
+def neural_forward_flops(n):
+    from paper_2505_08491_b200 import neural
+    m, q = n // 2, n // 4
+    f = 0.0
+    for name, op, cin, cout, ks, _ in neural.ARCHITECTURE:
+        if op == "tconv":
+            f += 2.0 * (m ** 3 if name == "up2" else n ** 3) * cin * cout
+        else:
+            vox = {"enc3": m ** 3, "dec2": m ** 3, "bottleneck": q ** 3}.get(name, n ** 3)
+            f += 2.0 * vox * cin * cout * ks ** 3
+    return f
 
 
 def spmv_roofline(solver, reps=50):
@@ -171,15 +260,7 @@ def spmv_roofline(solver, reps=50):
     p = solver.prob
     X = p.zeros().normal_()
     Y = p.zeros()
-    for _ in range(3):
-        solver.A.matvec(X, Y)
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(reps):
-        solver.A.matvec(X, Y)
-    e.record()
-    e.synchronize()
-    ms = s.elapsed_time(e) / reps
+    ms = device_ms(lambda: solver.A.matvec(X, Y), reps)
     nbytes = sum(16 * (p.n3 + int(n1)) for n1 in p.n1) + 40 * p.Qtot
     return ms, nbytes
 
@@ -343,6 +424,8 @@ def run_ours(args):
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
         }
+        if not args.no_target:
+            line["target_128"] = target_128(tf32, pk["hbm_gbs"])
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.workload, wl, iters)
         out = line
@@ -402,6 +485,7 @@ def main():
     ap.add_argument("--maxit", type=int, default=0)
     ap.add_argument("--ref-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-target", action="store_true", help="skip the 128^3 target-config rooflines")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -13,7 +13,7 @@ namespace mdp {
 enum OrthMode { DOT = 0, UPD_DOT = 1, UPD_NORM = 2, NORM = 3 };
 
 inline int red_blocks(int64_t n) {
-  int nb = ceil_div(n, 1024);
+  int nb = ceil_div(n, 512);
   int cap = 2 * sm_count();
   return nb < 1 ? 1 : (nb > cap ? cap : nb);
 }
@@ -39,24 +39,43 @@ __device__ __forceinline__ void finish_reduction(const double* __restrict__ part
                                                  unsigned int* ticket, const RedOut& R, const double* mine) {
   __shared__ bool last;
   const int i = blockIdx.y;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < R.nk) {
     double* dst = const_cast<double*>(partial) + ((int64_t)i * gridDim.x + blockIdx.x) * pstride;
-    for (int k = 0; k < R.nk; ++k) dst[k] = mine[k];
+    dst[threadIdx.x] = mine[threadIdx.x];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     __threadfence();
     last = atomicAdd(&ticket[i], 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // tpk threads per entry (a power of two <= 32, all in one warp), each
+  // summing a fixed block-strided subset with independent loads in flight,
+  // then a fixed xor-shuffle tree: the order depends on n and the SM count only
+  int tpk = 32;
+  while (tpk > 1 && tpk * R.nk > (int)blockDim.x) tpk >>= 1;
+  const int k = threadIdx.x / tpk, j = threadIdx.x % tpk;
   const double* base = partial + (int64_t)i * gridDim.x * pstride;
-  for (int k = wid; k < R.nk; k += nw) {
-    double t = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) t += __ldcg(base + (int64_t)b * pstride + k);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if (lane == 0) R.out[i * R.ostride + k] = R.mode == 1 ? sqrt(t) : t;
+  const int nblk = gridDim.x;
+  double t = 0.0;
+  if (k < R.nk) {
+    int b = j;
+    for (; b + 3 * tpk < nblk; b += 4 * tpk) {
+      const double p0 = __ldcg(base + (int64_t)b * pstride + k);
+      const double p1 = __ldcg(base + (int64_t)(b + tpk) * pstride + k);
+      const double p2 = __ldcg(base + (int64_t)(b + 2 * tpk) * pstride + k);
+      const double p3 = __ldcg(base + (int64_t)(b + 3 * tpk) * pstride + k);
+      t += p0;
+      t += p1;
+      t += p2;
+      t += p3;
+    }
+    for (; b < nblk; b += tpk) t += __ldcg(base + (int64_t)b * pstride + k);
   }
+  for (int o = tpk >> 1; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (k < R.nk && j == 0) R.out[i * R.ostride + k] = R.mode == 1 ? sqrt(t) : t;
   if (R.mode == 2) {  // hcol[k] = h1 + h2 (k < nv), hcol[kmax+1] = ||w||
     __syncthreads();
     const int nv = R.nvs[i];
@@ -65,6 +84,36 @@ __device__ __forceinline__ void finish_reduction(const double* __restrict__ part
     if (threadIdx.x == 0) R.hcol[i * (R.kmax + 2) + R.kmax + 1] = sqrt(R.out[i * R.ostride]);
   }
   if (threadIdx.x == 0) ticket[i] = 0u;
+}
+
+// Sum each of N per-lane values over the warp.  N >= 32: transpose
+// reduction (31 shuffles per 32 values), afterwards lane l holds the sum of
+// value (g * 32 + l) in v[g * 32]; N < 32: one xor tree per value, every lane
+// holds every sum.  Fixed order either way.
+template <int N>
+__device__ __forceinline__ void warp_sums(double* v) {
+  if constexpr (N >= 32) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int g = 0; g < N / 32; ++g) {
+      double* u = v + g * 32;
+#pragma unroll
+      for (int off = 16, cnt = 16; off >= 1; off >>= 1, cnt >>= 1) {
+        const bool upper = lane & off;
+#pragma unroll
+        for (int j = 0; j < cnt; ++j) {
+          const double send = upper ? u[j] : u[j + cnt];
+          const double keep = upper ? u[j + cnt] : u[j];
+          u[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < N; ++k)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  }
 }
 
 // One pass over V[0..nv) and w for a block's chunk of elements.
@@ -80,9 +129,10 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
                                                          const double* __restrict__ coef, int cstride,
                                                          double* __restrict__ partial, int pstride,
                                                          unsigned int* ticket, RedOut R) {
-  __shared__ double sh[32];
+  constexpr int NACC = (MODE == DOT || MODE == UPD_DOT) ? (NV > 0 ? NV : 1) : 1;
   __shared__ double csh[NV > 0 ? NV : 1];
-  __shared__ double mine[NV > 0 ? NV : 1];
+  __shared__ double wsum[4][NACC];
+  __shared__ double mine[NACC];
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
   const int nv = nvs ? nvs[i] : 0;
@@ -94,7 +144,6 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
     for (int k = threadIdx.x; k < NV; k += blockDim.x) csh[k] = k < nv ? coef[i * cstride + k] : 0.0;
     __syncthreads();
   }
-  constexpr int NACC = (MODE == DOT || MODE == UPD_DOT) ? (NV > 0 ? NV : 1) : 1;
   double acc[NACC];
 #pragma unroll
   for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
@@ -115,12 +164,19 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
     }
   }
   const int nk = (NACC > 1) ? nv : 1;
+  warp_sums<NACC>(acc);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if constexpr (NACC >= 32) {
 #pragma unroll
-  for (int k = 0; k < NACC; ++k) {
-    if (k >= nk) break;
-    double t = block_sum(acc[k], sh);
-    if (threadIdx.x == 0) mine[k] = t;
+    for (int g = 0; g < NACC / 32; ++g) wsum[wid][g * 32 + lane] = acc[g * 32];
+  } else {
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < NACC; ++k) wsum[wid][k] = acc[k];
   }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nk; k += blockDim.x)
+    mine[k] = ((wsum[0][k] + wsum[1][k]) + wsum[2][k]) + wsum[3][k];
   RedOut Rl = R;
   Rl.nk = nk;
   finish_reduction(partial, pstride, ticket, Rl, mine);

@@ -49,16 +49,20 @@ __global__ void __launch_bounds__(128) enc1a_kernel(const float2* __restrict__ x
 #pragma unroll
   for (int c = 0; c < 16; ++c) acc[c] = ws[864 + c];
   const float2* xb = xin + b * nvox;
-  for (int dz = 0; dz < 3; ++dz)
-    for (int dy = 0; dy < 3; ++dy)
-      for (int dx = 0; dx < 3; ++dx) {
-        int zz = z + dz - 1, yy = y + dy - 1, xx = x + dx - 1;
-        if (zz < 0 || yy < 0 || xx < 0 || zz >= S || yy >= S || xx >= S) continue;
-        float2 in = __ldg(xb + ((int64_t)zz * S + yy) * S + xx);
-        int tap = (dz * 3 + dy) * 3 + dx;
+  // all 27 neighbour loads are issued before any FMA (latency-bound otherwise);
+  // out-of-domain taps contribute exact zeros (same sums as skipping them)
+  float2 in[27];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) acc[c] += ws[(c * 2 + 0) * 27 + tap] * in.x + ws[(c * 2 + 1) * 27 + tap] * in.y;
-      }
+  for (int tap = 0; tap < 27; ++tap) {
+    const int zz = z + tap / 9 - 1, yy = y + (tap / 3) % 3 - 1, xx = x + tap % 3 - 1;
+    const bool ok = zz >= 0 && yy >= 0 && xx >= 0 && zz < S && yy < S && xx < S;
+    in[tap] = ok ? __ldg(xb + ((int64_t)zz * S + yy) * S + xx) : make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int tap = 0; tap < 27; ++tap)
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      acc[c] += ws[(c * 2 + 0) * 27 + tap] * in[tap].x + ws[(c * 2 + 1) * 27 + tap] * in[tap].y;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     float4 o = make_float4(fmaxf(acc[4 * q], 0.f), fmaxf(acc[4 * q + 1], 0.f), fmaxf(acc[4 * q + 2], 0.f),
@@ -146,69 +150,17 @@ __global__ void maxpool_kernel(const float4* __restrict__ in, int in_cq, int S, 
   }
 }
 
-// Transposed conv k=2 s=2 (neural.py:215-246) + bias + ReLU, output size
-// 2*Sin+op.  One block = one kernel tap (a,b,c) x 16 output channels over a
-// run of input voxels: the tap's weights (Cin x 16) sit in shared memory and
-// each input quad is read once, coalesced.  w packed [cout/16][cin][8][16].
-__global__ void __launch_bounds__(128) tconv_kernel(const float4* __restrict__ in, int in_cq, int cin,
-                                                     int Sin, int op, const float* __restrict__ w,
-                                                     const float* __restrict__ bias,
-                                                     float4* __restrict__ out, int out_cq, int out_q0,
-                                                     int round_tf32) {
-  __shared__ float4 wsh[128 * 4];  // [cin][16] for this tap
-  const int tap = blockIdx.y & 7, g = blockIdx.y >> 3, b = blockIdx.z;
-  const float* wg = w + (size_t)g * cin * 8 * 16;
-  for (int t = threadIdx.x; t < cin * 4; t += blockDim.x) {
-    const int ci = t >> 2, c4 = t & 3;
-    const float* src = wg + ((size_t)ci * 8 + tap) * 16 + 4 * c4;
-    wsh[t] = make_float4(src[0], src[1], src[2], src[3]);
-  }
-  __syncthreads();
-  const int So = 2 * Sin + op;
-  const int64_t nvo = (int64_t)So * So * So, nvi = (int64_t)Sin * Sin * Sin;
-  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (v >= nvi) return;
-  const int x = v % Sin, y = (v / Sin) % Sin, z = v / ((int64_t)Sin * Sin);
-  float acc[16];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) acc[c] = bias ? bias[g * 16 + c] : 0.f;
-  for (int q = 0; q < cin / 4; ++q) {
-    const float4 a = __ldg(in + ((int64_t)b * in_cq + q) * nvi + v);
-    const float av[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-#pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
-        const float4 wv = wsh[(4 * q + e) * 4 + c4];
-        acc[4 * c4] += av[e] * wv.x;
-        acc[4 * c4 + 1] += av[e] * wv.y;
-        acc[4 * c4 + 2] += av[e] * wv.z;
-        acc[4 * c4 + 3] += av[e] * wv.w;
-      }
-    }
-  }
-  const int X = 2 * x + (tap & 1), Y = 2 * y + ((tap >> 1) & 1), Z = 2 * z + (tap >> 2);
-  const int64_t o = ((int64_t)Z * So + Y) * So + X;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    float4 r = make_float4(fmaxf(acc[4 * q], 0.f), fmaxf(acc[4 * q + 1], 0.f), fmaxf(acc[4 * q + 2], 0.f),
-                           fmaxf(acc[4 * q + 3], 0.f));
-    if (round_tf32) r = tf32_round4(r);
-    out[((int64_t)b * out_cq + out_q0 + g * 4 + q) * nvo + o] = r;
-  }
-}
-
-// output-padding planes (index 2*Sin in any axis): relu(bias), no kernel mass
-__global__ void tconv_pad_kernel(int Sin, int cout, const float* __restrict__ bias, float4* __restrict__ out,
-                                 int out_cq, int out_q0, int nb, int round_tf32) {
+// output-padding planes (index 2*Sin in any axis): relu(bias), no kernel mass.
+// Run by the tail blocks of the tconv launch (blockIdx.y == 0 only).
+__device__ void tconv_pad(int Sin, int cout, const float* __restrict__ bias, float4* __restrict__ out,
+                          int out_cq, int out_q0, int b, int64_t t0, int64_t stride, int round_tf32) {
   const int So = 2 * Sin + 1, E = 2 * Sin;
   const int64_t nvo = (int64_t)So * So * So;
   const int64_t nplane = nvo - (int64_t)E * E * E;
-  const int64_t total = nplane * nb * (cout / 4);
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t total = nplane * (cout / 4);
+  for (int64_t t = t0; t < total; t += stride) {
     int64_t k = t % nplane;
-    const int64_t bq = t / nplane;
-    const int q = bq % (cout / 4), b = bq / (cout / 4);
+    const int q = t / nplane;
     // enumerate the voxels with max(X,Y,Z) == E: Z == E plane, then Y == E, then X == E
     int X, Y, Z;
     if (k < (int64_t)So * So) {
@@ -224,6 +176,71 @@ __global__ void tconv_pad_kernel(int Sin, int cout, const float* __restrict__ bi
                     : make_float4(0.f, 0.f, 0.f, 0.f);
     if (round_tf32) r = tf32_round4(r);
     out[((int64_t)b * out_cq + out_q0 + q) * nvo + ((int64_t)Z * So + Y) * So + X] = r;
+  }
+}
+
+// Transposed conv k=2 s=2 (neural.py:215-246) + bias + ReLU, output size
+// 2*Sin+op.  One block = one kernel tap (a,b,c) x 16 output channels over a
+// run of input voxels: the tap's weights (Cin x 16) sit in shared memory and
+// each input quad is read once, coalesced.  w packed [cout/16][cin][8][16].
+__global__ void __launch_bounds__(128) tconv_kernel(const float4* __restrict__ in, int in_cq, int cin,
+                                                     int Sin, int op, const float* __restrict__ w,
+                                                     const float* __restrict__ bias,
+                                                     float4* __restrict__ out, int out_cq, int out_q0,
+                                                     int round_tf32, int nmain) {
+  __shared__ float4 wsh[128 * 4];  // [cin][16] for this tap
+  const int tap = blockIdx.y & 7, g = blockIdx.y >> 3, b = blockIdx.z;
+  if ((int)blockIdx.x >= nmain) {  // tail blocks: the output-padding planes
+    if (blockIdx.y == 0)
+      tconv_pad(Sin, (int)(gridDim.y / 8) * 16, bias, out, out_cq, out_q0, b,
+                (blockIdx.x - nmain) * (int64_t)blockDim.x + threadIdx.x, (int64_t)(gridDim.x - nmain) * blockDim.x,
+                round_tf32);
+    return;
+  }
+  const float* wg = w + (size_t)g * cin * 8 * 16;
+  for (int t = threadIdx.x; t < cin * 4; t += blockDim.x) {
+    const int ci = t >> 2, c4 = t & 3;
+    const float* src = wg + ((size_t)ci * 8 + tap) * 16 + 4 * c4;
+    wsh[t] = make_float4(src[0], src[1], src[2], src[3]);
+  }
+  __syncthreads();
+  const int So = 2 * Sin + op;
+  const int64_t nvo = (int64_t)So * So * So, nvi = (int64_t)Sin * Sin * Sin;
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= nvi) return;
+  const int x = v % Sin, y = (v / Sin) % Sin, z = v / ((int64_t)Sin * Sin);
+  float acc[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) acc[c] = bias ? bias[g * 16 + c] : 0.f;
+  constexpr int QB = 8;  // input quads loaded per batch (cin/4 is a multiple of 8 here)
+  for (int q0 = 0; q0 < cin / 4; q0 += QB) {
+    float4 a[QB];
+#pragma unroll
+    for (int j = 0; j < QB; ++j) a[j] = __ldg(in + ((int64_t)b * in_cq + q0 + j) * nvi + v);
+#pragma unroll
+    for (int j = 0; j < QB; ++j) {
+      const float av[4] = {a[j].x, a[j].y, a[j].z, a[j].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const float4 wv = wsh[(4 * (q0 + j) + e) * 4 + c4];
+          acc[4 * c4] += av[e] * wv.x;
+          acc[4 * c4 + 1] += av[e] * wv.y;
+          acc[4 * c4 + 2] += av[e] * wv.z;
+          acc[4 * c4 + 3] += av[e] * wv.w;
+        }
+      }
+    }
+  }
+  const int X = 2 * x + (tap & 1), Y = 2 * y + ((tap >> 1) & 1), Z = 2 * z + (tap >> 2);
+  const int64_t o = ((int64_t)Z * So + Y) * So + X;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float4 r = make_float4(fmaxf(acc[4 * q], 0.f), fmaxf(acc[4 * q + 1], 0.f), fmaxf(acc[4 * q + 2], 0.f),
+                           fmaxf(acc[4 * q + 3], 0.f));
+    if (round_tf32) r = tf32_round4(r);
+    out[((int64_t)b * out_cq + out_q0 + g * 4 + q) * nvo + o] = r;
   }
 }
 
@@ -296,19 +313,19 @@ static int launch_pool(const float4* in, int in_cq, int S, int cq, float4* out, 
 static int launch_tconv(int nb, const float4* in, int in_cq, int cin, int cout, int Sin, int op, const float* w,
                         const float* bias, float4* out, int out_cq, int out_q0, int round_tf32,
                         cudaStream_t st) {
-  MDP_REQUIRE(cin <= 128 && cin % 4 == 0 && cout % 16 == 0, "tconv needs cin<=128, cin%%4==0, cout%%16==0");
+  MDP_REQUIRE(cin <= 128 && cin % 32 == 0 && cout % 16 == 0, "tconv needs cin<=128, cin%%32==0, cout%%16==0");
   const int64_t nvi = (int64_t)Sin * Sin * Sin;
-  dim3 grid(ceil_div(nvi, 128), 8 * (cout / 16), nb);
-  tconv_kernel<<<grid, 128, 0, st>>>(in, in_cq, cin, Sin, op, w, bias, out, out_cq, out_q0, round_tf32);
-  MDP_LAUNCH_CHECK("tconv_kernel");
+  const int nmain = ceil_div(nvi, 128);
+  int npad = 0;
   if (op) {
     const int So = 2 * Sin + 1;
-    const int64_t total = ((int64_t)So * So * So - 8 * nvi) * nb * (cout / 4);
-    int bx = ceil_div(total, 256);
-    bx = bx > 2 * sm_count() ? 2 * sm_count() : bx;
-    tconv_pad_kernel<<<bx, 256, 0, st>>>(Sin, cout, bias, out, out_cq, out_q0, nb, round_tf32);
-    MDP_LAUNCH_CHECK("tconv_pad_kernel");
+    const int64_t per_item = ((int64_t)So * So * So - 8 * nvi) * (cout / 4);
+    npad = ceil_div(per_item, 128);
+    npad = npad > 64 ? 64 : npad;
   }
+  dim3 grid(nmain + npad, 8 * (cout / 16), nb);
+  tconv_kernel<<<grid, 128, 0, st>>>(in, in_cq, cin, Sin, op, w, bias, out, out_cq, out_q0, round_tf32, nmain);
+  MDP_LAUNCH_CHECK("tconv_kernel");
   return MDP_OK;
 }
 

@@ -29,18 +29,8 @@ from paper_2505_08491_b200 import _ext, configs, neural  # noqa: E402
 
 
 def timed(fn, reps, flush):
-    ts = []
-    for _ in range(reps):
-        bench.flush_l2(flush)
-        torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        fn()
-        e.record()
-        e.synchronize()
-        ts.append(s.elapsed_time(e))
-    ts.sort()
-    return ts[len(ts) // 2]  # median ms
+    """Cold-L2 median device time; host enqueue hidden behind a GPU sleep (bench.device_ms)."""
+    return bench.device_ms(fn, reps, flush=flush, hide_us=2000)
 
 
 def main():
