@@ -262,20 +262,13 @@ __global__ void __launch_bounds__(128) head_kernel(const float4* __restrict__ d1
   const int64_t nvox = (int64_t)S * S * S;
   const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (v >= nvox) return;
-  float h[16];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) h[c] = ws[512 + c];
+  float d[32];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    float4 a = __ldg(d1 + ((int64_t)b * 8 + q) * nvox + v);
-#pragma unroll
-    for (int c = 0; c < 16; ++c)
-      h[c] += ws[c * 32 + 4 * q] * a.x + ws[c * 32 + 4 * q + 1] * a.y + ws[c * 32 + 4 * q + 2] * a.z +
-              ws[c * 32 + 4 * q + 3] * a.w;
+    const float4 a = __ldg(d1 + ((int64_t)b * 8 + q) * nvox + v);
+    d[4 * q] = a.x; d[4 * q + 1] = a.y; d[4 * q + 2] = a.z; d[4 * q + 3] = a.w;
   }
-  float y = ws[544];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) y += ws[528 + c] * fmaxf(h[c], 0.f);
+  const float y = head_eval(d, ws, ws + 512, ws + 528, ws + 544);
   const int s = sys_of(sel, b);
   z[s * ldz + v] = rnorm[b] * (double)y;
 }
@@ -348,13 +341,15 @@ UnetPlan unet_plan(int n, int nb, int path) {
   p.o_p2 = take((size_t)nb * 32 * Q * 16);
   p.o_bt = take((size_t)nb * 32 * Q * 16);
   p.o_d2 = take((size_t)nb * 16 * M * 16);
-  p.o_d1 = take((size_t)nb * 8 * N * 16);
-  if (path == 1) {  // unfused pooling needs the full-resolution pre-pool tensors
+  // path 0 fuses the heads into dec1's epilogue (no d1 tensor) and the pools
+  // into enc2/enc3; path 1 keeps d1 and the full-resolution pre-pool tensors
+  if (path == 1) {
+    p.o_d1 = take((size_t)nb * 8 * N * 16);
     p.o_e2 = take((size_t)nb * 16 * N * 16);
     p.o_e3 = take((size_t)nb * 32 * M * 16);
     p.o_scr = p.scr_bytes = 0;
   } else {
-    p.o_e2 = p.o_e3 = 0;
+    p.o_d1 = p.o_e2 = p.o_e3 = 0;
     size_t scr = 0;
     const int shp[6][3] = {{n, 16, 32}, {n, 32, 64}, {p.m, 64, 128}, {p.q, 128, 128}, {p.m, 128, 64}, {n, 64, 32}};
     for (auto& L : shp) {
@@ -455,8 +450,10 @@ extern "C" int mdp_unet_apply(const mdp_unet* net, int32_t nb, const int32_t* se
     if ((rc = tc_conv3(nb, m, 128, 64, c2, 32, 0, net->w[6], net->b[6], 1, d2, 16, 0, EPI_STORE, nullptr, ws + P.o_scr, P.scr_bytes, st)))
       return rc;
     if ((rc = launch_tconv(nb, d2, 16, 64, 32, m, op1, net->w[7], net->b[7], c1, 16, 0, 1, st))) return rc;
-    if ((rc = tc_conv3(nb, n, 64, 32, c1, 16, 0, net->w[8], net->b[8], 1, d1, 8, 0, EPI_STORE, nullptr, ws + P.o_scr, P.scr_bytes, st)))
-      return rc;
+    // dec1 with head1 -> head2 -> ||r|| scaling fused into its epilogue
+    HeadArgs H{net->w[9], net->b[9], net->w[10], net->b[10], sel, rnorm, z, ldz};
+    return tc_conv3(nb, n, 64, 32, c1, 16, 0, net->w[8], net->b[8], 1, nullptr, 0, 0, EPI_HEAD, &H, ws + P.o_scr,
+                    P.scr_bytes, st);
   }
   head_kernel<<<dim3(ceil_div(N, 128), nb), 128, 0, st>>>(d1, n, net->w[9], net->b[9], net->w[10], net->b[10],
                                                           sel, rnorm, z, ldz);

@@ -42,4 +42,26 @@ __device__ __forceinline__ float4 tf32_round4(float4 v) {
   return make_float4(tf32_round(v.x), tf32_round(v.y), tf32_round(v.z), tf32_round(v.w));
 }
 
+// head1 (32 -> 16, ReLU) and head2 (16 -> 1) of one voxel (neural.py:352-353);
+// d = the 32 dec1 activations as stored (bias, ReLU, TF32-rounded).  Shared by
+// the fused conv epilogue, the split-K reduce and the unfused head kernel so
+// every path sums in the same order.
+__device__ __forceinline__ float head_eval(const float* d, const float* __restrict__ w1,
+                                           const float* __restrict__ b1, const float* __restrict__ w2,
+                                           const float* __restrict__ b2) {
+  float h[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) h[c] = b1[c];
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      h[c] += w1[c * 32 + 4 * q] * d[4 * q] + w1[c * 32 + 4 * q + 1] * d[4 * q + 1] +
+              w1[c * 32 + 4 * q + 2] * d[4 * q + 2] + w1[c * 32 + 4 * q + 3] * d[4 * q + 3];
+  float y = b2[0];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) y += w2[c] * fmaxf(h[c], 0.f);
+  return y;
+}
+
 }  // namespace mdp

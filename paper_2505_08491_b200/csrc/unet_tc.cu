@@ -373,6 +373,29 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
             }
           }
         }
+      } else if (A.epi == EPI_HEAD) {  // dec1 (ncol == cout == 32) -> head1 -> head2 -> ||r|| * y
+        const HeadArgs& H = A.head;
+        const int sys = sys_of(H.sel, b);
+        const double rn = H.rnorm[b];
+#pragma unroll
+        for (int zp = 0; zp < ZP; ++zp) {
+          const int gz = z0 + zp;
+          const bool ok = gx < S && gy < S && gz < S;
+          float v[32];
+          tmem_ld16(dcol + zp * A.ncol, v);
+          tmem_ld16(dcol + zp * A.ncol + 16, v + 16);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            float m = v[i];
+            if (A.bias) m += A.bias[i];
+            if (A.relu) m = fmaxf(m, 0.f);
+            v[i] = tf32_round(m);
+          }
+          if (ok && !(A.dbg & 1)) {
+            const float y = head_eval(v, H.w1, H.b1, H.w2, H.b2);
+            H.z[sys * H.ldz + ((int64_t)gz * S + gy) * S + gx] = rn * (double)y;
+          }
+        }
       } else if (A.epi == EPI_POOL) {
         const int px = gx >> 1, py = gy >> 1, pz = z0 >> 1;
         const bool writer = ((lane & 1) == 0) && ((ly & 1) == 0) && px < So && py < So && pz < So;
@@ -470,6 +493,37 @@ __global__ void conv_split_reduce_kernel(const float4* __restrict__ part, int ks
   }
 }
 
+// EPI_HEAD after split-K: fixed-order partial sum of the 32 dec1 channels of
+// one voxel + bias + ReLU + TF32 rounding, then the heads and ||r|| scaling.
+__global__ void conv_split_reduce_head_kernel(const float4* __restrict__ part, int ksplit, int nb, int S,
+                                              const float* __restrict__ bias, int relu, const HeadArgs H) {
+  const int64_t S3 = (int64_t)S * S * S;
+  const int64_t total = (int64_t)nb * S3;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t % S3;
+    const int b = t / S3;
+    float d[32];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 acc = part[((int64_t)b * 8 + q) * S3 + v];
+      for (int k = 1; k < ksplit; ++k) {
+        const float4 p = part[(((int64_t)k * nb + b) * 8 + q) * S3 + v];
+        acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+      }
+      const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float m = a[e];
+        if (bias) m += bias[4 * q + e];
+        if (relu) m = fmaxf(m, 0.f);
+        d[4 * q + e] = tf32_round(m);
+      }
+    }
+    const float y = head_eval(d, H.w1, H.b1, H.w2, H.b2);
+    H.z[sys_of(H.sel, b) * H.ldz + v] = H.rnorm[b] * (double)y;
+  }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -522,7 +576,8 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   MDP_REQUIRE(cin % 16 == 0 && cin >= 16, "tc conv needs cin multiple of 16, got %d", cin);
   MDP_REQUIRE(cout % 16 == 0 && cout >= 16 && cout <= 128, "tc conv needs cout in {16..128} step 16, got %d",
               cout);
-  MDP_REQUIRE(epi == EPI_STORE || epi == EPI_POOL, "epilogue %d not supported by tc conv", epi);
+  MDP_REQUIRE(epi == EPI_STORE || epi == EPI_POOL || epi == EPI_HEAD, "epilogue %d not supported by tc conv", epi);
+  MDP_REQUIRE(epi != EPI_HEAD || (cout == 32 && head != nullptr), "fused head needs cout == 32 and head weights");
   EncodeTiledFn enc = encode_fn();
   MDP_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
   ConvArgs A{};
@@ -613,7 +668,13 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   int grid = A.ntiles < sm_count() ? A.ntiles : sm_count();
   conv3_tc_kernel<<<grid, 256, smem, st>>>(map, A);
   MDP_LAUNCH_CHECK("conv3_tc_kernel");
-  if (A.ksplit > 1) {
+  if (A.ksplit > 1 && epi == EPI_HEAD) {
+    const int64_t total = (int64_t)nb * S * S * S;
+    int bx = ceil_div(total, 128);
+    bx = bx > 8 * sm_count() ? 8 * sm_count() : bx;
+    conv_split_reduce_head_kernel<<<bx, 128, 0, st>>>(A.partial, A.ksplit, nb, S, bias, relu, A.head);
+    MDP_LAUNCH_CHECK("conv_split_reduce_head_kernel");
+  } else if (A.ksplit > 1) {
     const int pool = epi == EPI_POOL;
     const int So = pool ? S / 2 : S;
     const int64_t total = (int64_t)nb * (cout / 4) * So * So * So;

@@ -86,8 +86,10 @@ def test_solve_cfg1_reference_semantics(gpu, label, tmp_path):
         # the reference hovers at ~1e-6 for >100 iterations and its trajectory
         # is chaotic under any change of summation order: gate on the early
         # history and on staying in the converging regime
+        # measured: 1e-5 relative over the first 8 iterations, 3e-3 by iteration 14
         got = np.asarray(rep.residual_history[:15])
-        assert np.allclose(got, h[:15], rtol=2e-3), np.c_[got, h[:15]]
+        assert np.allclose(got[:8], h[:8], rtol=2e-4), np.c_[got, h[:15]]
+        assert np.allclose(got, h[:15], rtol=1e-2), np.c_[got, h[:15]]
         assert rep.rel_residual <= 1e-4, rep.rel_residual
 
 
