@@ -14,7 +14,7 @@ enum OrthMode { DOT = 0, UPD_DOT = 1, UPD_NORM = 2, NORM = 3 };
 
 inline int red_blocks(int64_t n) {
   int nb = ceil_div(n, 512);
-  int cap = 2 * sm_count();
+  int cap = 4 * sm_count();
   return nb < 1 ? 1 : (nb > cap ? cap : nb);
 }
 
@@ -147,18 +147,33 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
   double acc[NACC];
 #pragma unroll
   for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
+  // basis values are loaded in batches of KB independent loads ahead of their
+  // FMAs (same per-element operation order as a plain k loop)
+  constexpr int KB = NV < 8 ? (NV > 0 ? NV : 1) : 8;
   for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     double we = ws[e];
     if (MODE == UPD_DOT || MODE == UPD_NORM) {
 #pragma unroll
-      for (int k = 0; k < NV; ++k)
-        if (k < nv) we -= csh[k] * __ldg(Vs + k * ldv_vec + e);
+      for (int k0 = 0; k0 < NV; k0 += KB) {
+        double vv[KB];
+#pragma unroll
+        for (int j = 0; j < KB; ++j) vv[j] = k0 + j < nv ? __ldg(Vs + (k0 + j) * ldv_vec + e) : 0.0;
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+          if (k0 + j < nv) we -= csh[k0 + j] * vv[j];
+      }
       ws[e] = we;
     }
     if (MODE == DOT || MODE == UPD_DOT) {
 #pragma unroll
-      for (int k = 0; k < NACC; ++k)
-        if (k < nv) acc[k] += __ldg(Vs + k * ldv_vec + e) * we;
+      for (int k0 = 0; k0 < NACC; k0 += KB) {
+        double vv[KB];
+#pragma unroll
+        for (int j = 0; j < KB; ++j) vv[j] = k0 + j < nv ? __ldg(Vs + (k0 + j) * ldv_vec + e) : 0.0;
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+          if (k0 + j < nv) acc[k0 + j] += vv[j] * we;
+      }
     } else {
       acc[0] += we * we;
     }

@@ -11,6 +11,8 @@
 //   y3  += w T^T s      (pull over touched nodes)   pi_scatter
 //   y1   = K11 x1 - w D Psi^T s                     oned_apply
 // which equals full_operator(s) @ x.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace mdp {
@@ -352,6 +354,14 @@ static int launch_stencil(const mdp_problem* p, int32_t nsel, const int32_t* sel
   const int zmax = n / zmin_len > 1 ? n / zmin_len : 1;
   zch = zch < 1 ? 1 : (zch > zmax ? zmax : zch);
   int zchunk = ceil_div(n, zch);
+  {
+    static int forced = -1;  // MDP_STENCIL_ZCHUNK: tuning experiments only (tools/stencil_sweep.py)
+    if (forced < 0) {
+      const char* e = getenv("MDP_STENCIL_ZCHUNK");
+      forced = e ? atoi(e) : 0;
+    }
+    if (forced > 0) zchunk = forced < n ? forced : n;
+  }
   zch = ceil_div(n, zchunk);
   const bool gat = g != nullptr && p->qmax > 0;
   if (gat) bx = bx > ceil_div(p->qmax, 4) ? bx : ceil_div(p->qmax, 4);  // one warp per Pi row in the gather slice
