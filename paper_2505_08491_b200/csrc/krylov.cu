@@ -12,9 +12,19 @@ namespace mdp {
 
 enum OrthMode { DOT = 0, UPD_DOT = 1, UPD_NORM = 2, NORM = 3 };
 
+#ifndef ORTH_CAP
+#define ORTH_CAP 2
+#endif
+#ifndef ORTH_VEC
+#define ORTH_VEC 2
+#endif
+#ifndef ORTH_KB
+#define ORTH_KB 8
+#endif
+
 inline int red_blocks(int64_t n) {
   int nb = ceil_div(n, 512);
-  int cap = 4 * sm_count();
+  int cap = ORTH_CAP * sm_count();
   return nb < 1 ? 1 : (nb > cap ? cap : nb);
 }
 
@@ -136,7 +146,7 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
   const int nv = nvs ? nvs[i] : 0;
-  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t chunk = ((n + gridDim.x - 1) / gridDim.x + 1) & ~(int64_t)1;  // even: 16-byte aligned pairs
   const int64_t e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
   const double* Vs = V ? V + s * ldv_sys : nullptr;
   double* ws = w + s * ldw;
@@ -147,35 +157,79 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
   double acc[NACC];
 #pragma unroll
   for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
-  // basis values are loaded in batches of KB independent loads ahead of their
-  // FMAs (same per-element operation order as a plain k loop)
-  constexpr int KB = NV < 8 ? (NV > 0 ? NV : 1) : 8;
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    double we = ws[e];
-    if (MODE == UPD_DOT || MODE == UPD_NORM) {
+  // Each thread walks element pairs (16-byte loads: longer contiguous runs per
+  // basis vector per warp), the basis values of one element batch loaded in
+  // groups of KB independent loads ahead of their FMAs.  Per element the
+  // operation order is that of a plain k loop.
+  constexpr int KB = NV < ORTH_KB ? (NV > 0 ? NV : 1) : ORTH_KB;
+  for (int64_t e = e0 + ORTH_VEC * threadIdx.x; e < e1; e += ORTH_VEC * blockDim.x) {
+    if (ORTH_VEC == 2 && e + 1 < e1) {
+      double2 w2 = *reinterpret_cast<const double2*>(ws + e);
+      if (MODE == UPD_DOT || MODE == UPD_NORM) {
 #pragma unroll
-      for (int k0 = 0; k0 < NV; k0 += KB) {
-        double vv[KB];
+        for (int k0 = 0; k0 < NV; k0 += KB) {
+          double2 vv[KB];
 #pragma unroll
-        for (int j = 0; j < KB; ++j) vv[j] = k0 + j < nv ? __ldg(Vs + (k0 + j) * ldv_vec + e) : 0.0;
+          for (int j = 0; j < KB; ++j)
+            vv[j] = k0 + j < nv ? __ldg(reinterpret_cast<const double2*>(Vs + (k0 + j) * ldv_vec + e))
+                                : make_double2(0.0, 0.0);
 #pragma unroll
-        for (int j = 0; j < KB; ++j)
-          if (k0 + j < nv) we -= csh[k0 + j] * vv[j];
+          for (int j = 0; j < KB; ++j)
+            if (k0 + j < nv) {
+              w2.x -= csh[k0 + j] * vv[j].x;
+              w2.y -= csh[k0 + j] * vv[j].y;
+            }
+        }
+        *reinterpret_cast<double2*>(ws + e) = w2;
       }
-      ws[e] = we;
+      if (MODE == DOT || MODE == UPD_DOT) {
+#pragma unroll
+        for (int k0 = 0; k0 < NACC; k0 += KB) {
+          double2 vv[KB];
+#pragma unroll
+          for (int j = 0; j < KB; ++j)
+            vv[j] = k0 + j < nv ? __ldg(reinterpret_cast<const double2*>(Vs + (k0 + j) * ldv_vec + e))
+                                : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int j = 0; j < KB; ++j)
+            if (k0 + j < nv) {
+              acc[k0 + j] += vv[j].x * w2.x;
+              acc[k0 + j] += vv[j].y * w2.y;
+            }
+        }
+      } else {
+        acc[0] += w2.x * w2.x;
+        acc[0] += w2.y * w2.y;
+      }
+      continue;
     }
-    if (MODE == DOT || MODE == UPD_DOT) {
+    for (int64_t f = e; f < e + ORTH_VEC && f < e1; ++f) {
+      double we = ws[f];
+      if (MODE == UPD_DOT || MODE == UPD_NORM) {
 #pragma unroll
-      for (int k0 = 0; k0 < NACC; k0 += KB) {
-        double vv[KB];
+        for (int k0 = 0; k0 < NV; k0 += KB) {
+          double vv[KB];
 #pragma unroll
-        for (int j = 0; j < KB; ++j) vv[j] = k0 + j < nv ? __ldg(Vs + (k0 + j) * ldv_vec + e) : 0.0;
+          for (int j = 0; j < KB; ++j) vv[j] = k0 + j < nv ? __ldg(Vs + (k0 + j) * ldv_vec + f) : 0.0;
 #pragma unroll
-        for (int j = 0; j < KB; ++j)
-          if (k0 + j < nv) acc[k0 + j] += vv[j] * we;
+          for (int j = 0; j < KB; ++j)
+            if (k0 + j < nv) we -= csh[k0 + j] * vv[j];
+        }
+        ws[f] = we;
       }
-    } else {
-      acc[0] += we * we;
+      if (MODE == DOT || MODE == UPD_DOT) {
+#pragma unroll
+        for (int k0 = 0; k0 < NACC; k0 += KB) {
+          double vv[KB];
+#pragma unroll
+          for (int j = 0; j < KB; ++j) vv[j] = k0 + j < nv ? __ldg(Vs + (k0 + j) * ldv_vec + f) : 0.0;
+#pragma unroll
+          for (int j = 0; j < KB; ++j)
+            if (k0 + j < nv) acc[k0 + j] += vv[j] * we;
+        }
+      } else {
+        acc[0] += we * we;
+      }
     }
   }
   const int nk = (NACC > 1) ? nv : 1;
@@ -505,6 +559,8 @@ extern "C" int mdp_arnoldi(int32_t nsel, const int32_t* sel, double* V, int64_t 
                            void* stream) {
   MDP_REQUIRE(kmax >= 1 && kmax <= 63, "kmax %d outside [1, 63]", kmax);
   MDP_REQUIRE(n > 0, "empty vectors");
+  MDP_REQUIRE(((uintptr_t)V | (uintptr_t)w) % 16 == 0 && (ldv_sys | ldv_vec | ldw) % 2 == 0,
+              "V and w must be 16-byte aligned with even strides (element pairs are loaded as double2)");
   if (nsel == 0) return MDP_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = red_blocks(n);
@@ -544,6 +600,7 @@ extern "C" int mdp_norms(int32_t nsel, const int32_t* sel, const double* x, int6
                          double* out, void* work, void* stream) {
   if (nsel == 0) return MDP_OK;
   MDP_REQUIRE(n > 0, "empty vectors");
+  MDP_REQUIRE((uintptr_t)x % 16 == 0 && ldx % 2 == 0, "x must be 16-byte aligned with an even stride");
   cudaStream_t st = (cudaStream_t)stream;
   const int nb = red_blocks(n);
   Work W = carve(work, nsel, 1, n);

@@ -150,35 +150,6 @@ __global__ void maxpool_kernel(const float4* __restrict__ in, int in_cq, int S, 
   }
 }
 
-// output-padding planes (index 2*Sin in any axis): relu(bias), no kernel mass.
-// Run by the tail blocks of the tconv launch (blockIdx.y == 0 only).
-__device__ void tconv_pad(int Sin, int cout, const float* __restrict__ bias, float4* __restrict__ out,
-                          int out_cq, int out_q0, int b, int64_t t0, int64_t stride, int round_tf32) {
-  const int So = 2 * Sin + 1, E = 2 * Sin;
-  const int64_t nvo = (int64_t)So * So * So;
-  const int64_t nplane = nvo - (int64_t)E * E * E;
-  const int64_t total = nplane * (cout / 4);
-  for (int64_t t = t0; t < total; t += stride) {
-    int64_t k = t % nplane;
-    const int q = t / nplane;
-    // enumerate the voxels with max(X,Y,Z) == E: Z == E plane, then Y == E, then X == E
-    int X, Y, Z;
-    if (k < (int64_t)So * So) {
-      Z = E; Y = k / So; X = k % So;
-    } else if ((k -= (int64_t)So * So) < (int64_t)E * So) {
-      Z = k / So; Y = E; X = k % So;
-    } else {
-      k -= (int64_t)E * So;
-      Z = k / E; Y = k % E; X = E;
-    }
-    float4 r = bias ? make_float4(fmaxf(bias[4 * q], 0.f), fmaxf(bias[4 * q + 1], 0.f), fmaxf(bias[4 * q + 2], 0.f),
-                                  fmaxf(bias[4 * q + 3], 0.f))
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
-    if (round_tf32) r = tf32_round4(r);
-    out[((int64_t)b * out_cq + out_q0 + q) * nvo + ((int64_t)Z * So + Y) * So + X] = r;
-  }
-}
-
 // Transposed conv k=2 s=2 (neural.py:215-246) + bias + ReLU, output size
 // 2*Sin+op.  One block = one kernel tap (a,b,c) x 16 output channels over a
 // run of input voxels: the tap's weights (Cin x 16) sit in shared memory and
@@ -446,10 +417,10 @@ extern "C" int mdp_unet_apply(const mdp_unet* net, int32_t nb, const int32_t* se
       return rc;
     if ((rc = tc_conv3(nb, q, 128, 128, p2, 32, 0, net->w[4], nullptr, 1, bt, 32, 0, EPI_STORE, nullptr, ws + P.o_scr, P.scr_bytes, st)))
       return rc;
-    if ((rc = launch_tconv(nb, bt, 32, 128, 64, q, op2, net->w[5], nullptr, c2, 32, 0, 1, st))) return rc;
+    if ((rc = tc_tconv(nb, bt, 32, 128, 64, q, op2, net->w[5], nullptr, c2, 32, 0, st))) return rc;
     if ((rc = tc_conv3(nb, m, 128, 64, c2, 32, 0, net->w[6], net->b[6], 1, d2, 16, 0, EPI_STORE, nullptr, ws + P.o_scr, P.scr_bytes, st)))
       return rc;
-    if ((rc = launch_tconv(nb, d2, 16, 64, 32, m, op1, net->w[7], net->b[7], c1, 16, 0, 1, st))) return rc;
+    if ((rc = tc_tconv(nb, d2, 16, 64, 32, m, op1, net->w[7], net->b[7], c1, 16, 0, st))) return rc;
     // dec1 with head1 -> head2 -> ||r|| scaling fused into its epilogue
     HeadArgs H{net->w[9], net->b[9], net->w[10], net->b[10], sel, rnorm, z, ldz};
     return tc_conv3(nb, n, 64, 32, c1, 16, 0, net->w[8], net->b[8], 1, nullptr, 0, 0, EPI_HEAD, &H, ws + P.o_scr,

@@ -30,6 +30,10 @@ struct HeadArgs {  // dec1 -> head1 -> head2 -> scale (EPI_HEAD)
 int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int in_q0, const float* w,
              const float* bias, int relu, float4* out, int out_cq, int out_q0, int epi, const HeadArgs* head,
              void* scratch, size_t scratch_bytes, cudaStream_t st);
+// transposed conv k=2 s=2 (+ bias, ReLU, TF32 rounding, output-padding
+// planes) on tensor cores; w packed [tap][quad][Cout][4] (neural.pack_tconv path 0)
+int tc_tconv(int nb, const float4* in, int in_cq, int cin, int cout, int Sin, int op, const float* w,
+             const float* bias, float4* out, int out_cq, int out_q0, cudaStream_t st);
 // scratch needed by the split-K partial sums of one layer (0 when not split)
 size_t tc_conv3_scratch_bytes(int nb, int S, int cin, int cout);
 
@@ -40,6 +44,35 @@ __device__ __forceinline__ float tf32_round(float f) {
 }
 __device__ __forceinline__ float4 tf32_round4(float4 v) {
   return make_float4(tf32_round(v.x), tf32_round(v.y), tf32_round(v.z), tf32_round(v.w));
+}
+
+// output-padding planes (index 2*Sin in any axis): relu(bias), no kernel mass.
+// Run by the tail blocks of the tconv launches (one tap group only).
+__device__ __forceinline__ void tconv_pad(int Sin, int cout, const float* __restrict__ bias, float4* __restrict__ out,
+                          int out_cq, int out_q0, int b, int64_t t0, int64_t stride, int round_tf32) {
+  const int So = 2 * Sin + 1, E = 2 * Sin;
+  const int64_t nvo = (int64_t)So * So * So;
+  const int64_t nplane = nvo - (int64_t)E * E * E;
+  const int64_t total = nplane * (cout / 4);
+  for (int64_t t = t0; t < total; t += stride) {
+    int64_t k = t % nplane;
+    const int q = t / nplane;
+    // enumerate the voxels with max(X,Y,Z) == E: Z == E plane, then Y == E, then X == E
+    int X, Y, Z;
+    if (k < (int64_t)So * So) {
+      Z = E; Y = k / So; X = k % So;
+    } else if ((k -= (int64_t)So * So) < (int64_t)E * So) {
+      Z = k / So; Y = E; X = k % So;
+    } else {
+      k -= (int64_t)E * So;
+      Z = k / E; Y = k % E; X = E;
+    }
+    float4 r = bias ? make_float4(fmaxf(bias[4 * q], 0.f), fmaxf(bias[4 * q + 1], 0.f), fmaxf(bias[4 * q + 2], 0.f),
+                                  fmaxf(bias[4 * q + 3], 0.f))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (round_tf32) r = tf32_round4(r);
+    out[((int64_t)b * out_cq + out_q0 + q) * nvo + ((int64_t)Z * So + Y) * So + X] = r;
+  }
 }
 
 // head1 (32 -> 16, ReLU) and head2 (16 -> 1) of one voxel (neural.py:352-353);

@@ -524,6 +524,118 @@ __global__ void conv_split_reduce_head_kernel(const float4* __restrict__ part, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Transposed conv k=2 s=2 (neural.py:215-246) as tcgen05 GEMMs: every output
+// voxel takes exactly one tap, so per tap it is [input voxels x Cin] x [Cin x
+// Cout].  CTA = 128 consecutive input voxels (one M=128 block) x a group of
+// tg taps: the voxels' Cin channels (cin/4 quad rows of 2 KB, 1-D bulk
+// copies, K-major core matrices of 8 voxels x 16 B) and the group's weights
+// ([tap][quad][Cout][4]) land in shared memory once; one MMA chain per tap
+// accumulates into its own TMEM columns; the four warps then read their 32
+// TMEM lanes and scatter each tap's row to output voxel (2x+a, 2y+b, 2z+c).
+// Tail blocks write the output-padding planes.
+struct TconvArgs {
+  const float4* in;
+  int in_cq, cin, cout, Sin, op, tg, nmain;
+  const float* w;
+  const float* bias;
+  float4* out;
+  int out_cq, out_q0;
+  uint32_t a_bytes, b_bytes, tmem_cols;
+};
+
+__global__ void __launch_bounds__(128, 1) tconv_tc_kernel(const TconvArgs T) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int b = blockIdx.z, grp = blockIdx.y;
+  if ((int)blockIdx.x >= T.nmain) {  // tail blocks: output-padding planes
+    if (grp == 0)
+      tconv_pad(T.Sin, T.cout, T.bias, T.out, T.out_cq, T.out_q0, b,
+                (blockIdx.x - T.nmain) * (int64_t)blockDim.x + threadIdx.x,
+                (int64_t)(gridDim.x - T.nmain) * blockDim.x, 1);
+    return;
+  }
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + T.a_bytes;
+  uint64_t* full = (uint64_t*)(sB + T.b_bytes);
+  uint64_t* done = full + 1;
+  uint32_t* tmem_slot = (uint32_t*)(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Sin = T.Sin;
+  const int64_t nvi = (int64_t)Sin * Sin * Sin;
+  const int64_t v0 = (int64_t)blockIdx.x * 128;
+  const int nvox = (int)(nvi - v0 < 128 ? nvi - v0 : 128);
+  const int nq = T.cin / 4;
+  if (threadIdx.x == 0) {
+    mbar_init(full, 1);
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(T.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) {
+    const uint32_t rowb = (uint32_t)nvox * 16u;
+    mbar_expect_tx(full, rowb * nq + T.b_bytes);
+    for (int q = 0; q < nq; ++q)
+      bulk_load(sA + (size_t)q * 2048, T.in + ((int64_t)b * T.in_cq + q) * nvi + v0, rowb, full);
+    bulk_load(sB, T.w + (size_t)grp * T.tg * T.cin * T.cout, T.b_bytes, full);
+    mbar_wait(full, 0);
+    fence_after();
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(T.cout >> 3) << 17) |
+                           ((uint32_t)(128 >> 4) << 24);
+    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+    for (int t = 0; t < T.tg; ++t)
+      for (int ks = 0; ks < nq / 2; ++ks) {
+        const uint64_t ad = umma_desc(a0 + ks * 2 * 2048, 2048, 128);
+        const uint64_t bd = umma_desc(b0 + (uint32_t)((t * nq + 2 * ks) * T.cout * 16), T.cout * 16, 128);
+        mma_tf32(tmem + (uint32_t)(t * T.cout), ad, bd, idesc, ks > 0 ? 1u : 0u);
+      }
+    mma_commit(done);
+  }
+  __syncwarp();
+  mbar_wait(done, 0);
+  fence_after();
+  // epilogue: warp w owns TMEM lanes (= voxel rows) 32w..32w+31
+  const int row = warp * 32 + lane;
+  const int64_t v = v0 + row;
+  const bool live = row < nvox;
+  const int x = live ? (int)(v % Sin) : 0, y = live ? (int)((v / Sin) % Sin) : 0,
+            z = live ? (int)(v / ((int64_t)Sin * Sin)) : 0;
+  const int So = 2 * Sin + T.op;
+  const int64_t nvo = (int64_t)So * So * So;
+  const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
+  for (int t = 0; t < T.tg; ++t) {
+    const int tap = grp * T.tg + t;
+    const int64_t o = ((int64_t)(2 * z + (tap >> 2)) * So + 2 * y + ((tap >> 1) & 1)) * So + 2 * x + (tap & 1);
+    for (int cg = 0; cg < T.cout / 16; ++cg) {
+      float r[16];
+      tmem_ld16(tmem + lane_addr + (uint32_t)(t * T.cout + cg * 16), r);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float m = r[i];
+        if (T.bias) m += T.bias[cg * 16 + i];
+        r[i] = tf32_round(fmaxf(m, 0.f));
+      }
+      if (live)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          T.out[((int64_t)b * T.out_cq + T.out_q0 + cg * 4 + q) * nvo + o] =
+              make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(T.tmem_cols));
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -684,6 +796,53 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
                                                  out_cq, out_q0);
     MDP_LAUNCH_CHECK("conv_split_reduce_kernel");
   }
+  return MDP_OK;
+}
+
+int tc_tconv(int nb, const float4* in, int in_cq, int cin, int cout, int Sin, int op, const float* w,
+             const float* bias, float4* out, int out_cq, int out_q0, cudaStream_t st) {
+  using namespace tc;
+  MDP_REQUIRE(cin % 8 == 0 && cin <= 128 && cout % 16 == 0 && cout <= 128, "tc tconv needs cin%%8==0 (<=128), "
+              "cout%%16==0 (<=128), got %d/%d", cin, cout);
+  TconvArgs T{};
+  T.in = in;
+  T.in_cq = in_cq;
+  T.cin = cin;
+  T.cout = cout;
+  T.Sin = Sin;
+  T.op = op;
+  T.w = w;
+  T.bias = bias;
+  T.out = out;
+  T.out_cq = out_cq;
+  T.out_q0 = out_q0;
+  T.a_bytes = (uint32_t)cin * 128 * 4;
+  const size_t budget = 200 * 1024;
+  int tg = 8;
+  while (tg > 1 && ((size_t)T.a_bytes + (size_t)tg * cin * cout * 4 > budget || tg * cout > 256)) tg >>= 1;
+  T.tg = tg;
+  T.b_bytes = (uint32_t)(tg * cin * cout * 4);
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(tg * cout)) cols <<= 1;
+  T.tmem_cols = cols;
+  const int64_t nvi = (int64_t)Sin * Sin * Sin;
+  T.nmain = ceil_div(nvi, 128);
+  int npad = 0;
+  if (op) {
+    const int So = 2 * Sin + 1;
+    const int64_t per_item = ((int64_t)So * So * So - 8 * nvi) * (cout / 4);
+    npad = ceil_div(per_item, 128);
+    npad = npad > 64 ? 64 : npad;
+  }
+  const size_t smem = 1024 + (size_t)T.a_bytes + T.b_bytes + 64;
+  static size_t attr_set = 0;
+  if (attr_set < smem) {
+    cudaFuncSetAttribute(tconv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+    attr_set = 227 * 1024;
+  }
+  dim3 grid(T.nmain + npad, 8 / tg, nb);
+  tconv_tc_kernel<<<grid, 128, smem, st>>>(T);
+  MDP_LAUNCH_CHECK("tconv_tc_kernel");
   return MDP_OK;
 }
 

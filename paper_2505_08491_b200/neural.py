@@ -174,11 +174,15 @@ def pack_conv(kernel: np.ndarray, path: int) -> np.ndarray:
     return tf32_round(np.ascontiguousarray(p))
 
 
-def pack_tconv(kernel: np.ndarray) -> np.ndarray:
-    """(Cin, Cout, 2, 2, 2) -> [Cout/16][Cin][8][16]."""
+def pack_tconv(kernel: np.ndarray, path: int = 1) -> np.ndarray:
+    """(Cin, Cout, 2, 2, 2) -> path 1 (CUDA cores): [Cout/16][Cin][8][16];
+    path 0 (tcgen05): [tap][quad][Cout][4], TF32-rounded (tap = 4a + 2b + c)."""
     cin, cout = kernel.shape[:2]
-    k = np.asarray(kernel, dtype=np.float32).reshape(cin, cout // 16, 16, 8)
-    return np.ascontiguousarray(k.transpose(1, 0, 3, 2))
+    if path == PATH_CUDA_CORE:
+        k = np.asarray(kernel, dtype=np.float32).reshape(cin, cout // 16, 16, 8)
+        return np.ascontiguousarray(k.transpose(1, 0, 3, 2))
+    k = np.asarray(kernel, dtype=np.float32).reshape(cin // 4, 4, cout, 8)
+    return tf32_round(np.ascontiguousarray(k.transpose(3, 0, 2, 1)))
 
 
 class DeviceUNet:
@@ -198,7 +202,7 @@ class DeviceUNet:
             if name == "enc1a":
                 w = np.asarray(k, dtype=np.float32).reshape(16, 2, 27)
             elif op == "tconv":
-                w = pack_tconv(k)
+                w = pack_tconv(k, path)
             elif ks == 1:
                 w = np.asarray(k, dtype=np.float32).reshape(cout, cin)
             else:

@@ -100,3 +100,5 @@ def test_weight_packing_layouts():
     t = rng.standard_normal((64, 32, 2, 2, 2)).astype(np.float32)
     pt = neural.pack_tconv(t).reshape(2, 64, 8, 16)
     assert pt[1, 10, 5, 3] == t[10, 16 + 3].ravel()[5]
+    p0 = neural.pack_tconv(t, neural.PATH_TCGEN05).reshape(8, 16, 32, 4)  # [tap][quad][cout][4]
+    assert abs(p0[5, 3, 17, 2] - t[3 * 4 + 2, 17].ravel()[5]) <= 1e-3 * abs(t[14, 17].ravel()[5])

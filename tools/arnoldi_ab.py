@@ -1,6 +1,6 @@
 """A/B timing of mdp_arnoldi between the current library and another build.
 
-    python tools/arnoldi_ab.py tools/ab/libold.so
+    python tools/arnoldi_ab.py tools/ab/libold.so [more.so ...]
 """
 import ctypes as C
 import sys
@@ -18,7 +18,9 @@ def load(path):
     return lib
 
 
-libs = {"new": _ext.lib(), "old": load(sys.argv[1])}
+libs = {"cur": _ext.lib()}
+for path in sys.argv[1:]:
+    libs[path.rsplit("/", 1)[-1].replace(".so", "")] = load(path)
 flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device="cuda")
 for n, nb, k in [(36000, 1, 30), (36000, 1, 4), (2146689, 1, 30), (2146689, 8, 30), (7189057, 1, 30), (274625, 16, 50)]:
     ld = (n + 31) // 32 * 32
