@@ -12,8 +12,10 @@ namespace mdp {
 
 enum OrthMode { DOT = 0, UPD_DOT = 1, UPD_NORM = 2, NORM = 3 };
 
+// orth-pass tuning (tools/arnoldi_ab.py, profiles/): blocks per SM cap, elements per
+// thread step (2 = 16-byte loads), independent basis loads per batch
 #ifndef ORTH_CAP
-#define ORTH_CAP 2
+#define ORTH_CAP 4
 #endif
 #ifndef ORTH_VEC
 #define ORTH_VEC 2

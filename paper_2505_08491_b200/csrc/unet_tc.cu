@@ -52,7 +52,8 @@ struct ConvArgs {
   uint32_t a_bytes, b_bytes;
   int na, nbs;
   int resident;  // 1: the whole filter (27 taps, one chunk) stays in shared memory
-  int tps;       // taps per weight stage (one mbarrier handshake per stage)
+  int tps;       // taps (fold: (dy,dx) units) per weight stage (one mbarrier handshake per stage)
+  int fold;      // Cout == 32: the 3 z-taps of one (dy,dx) are one N = 3*32 weight block (see issue_stage_fold)
   int dbg;       // MDP_DEBUG_CONV bits (timing experiments only): 1 no stores, 2 no MMA, 4 no TMA, 8 no weight copies
   uint32_t tmem_cols;
   HeadArgs head;
@@ -151,6 +152,41 @@ __device__ __forceinline__ void issue_stage(uint32_t a_lo, uint32_t a_hi, uint32
   }
 }
 
+// Start-address offset (16-byte units) of (dy,dx) unit u's view of halo plane 0.
+__host__ __device__ constexpr uint32_t unit_off16(int u) { return (uint32_t)((u / 3) * HX + u % 3); }
+
+// z-tap fold for Cout = 32 layers (A-operand-read bound at N = 32): for one
+// (dy,dx) shift, halo plane hp feeds output plane zp through z-tap dz = hp - zp,
+// so one A read serves both output planes with N = 2*32 (hp = 1, 2) or one
+// plane with N = 32 (hp = 0, 3).  Weights per unit are [quad][dz][Cout][4], so a
+// dz range is a contiguous N range; accumulators are stored descending in zp
+// (plane zp at column (ZP-1-zp)*ncol) so every MMA's D is one contiguous range.
+// hp = 1 goes first: it covers both accumulators, so the tile's first MMA
+// (accumulate = 0) initialises all of D.
+template <int TPS>
+__device__ __forceinline__ void issue_stage_fold(uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi,
+                                                 uint32_t b_unit16, uint32_t b_ks16, uint32_t dcol, uint32_t ncol,
+                                                 uint32_t idesc1, uint32_t idesc2, uint32_t& accf) {
+  static_assert(ZP == 2, "fold schedule assumes two output planes per brick");
+#pragma unroll
+  for (int tt = 0; tt < TPS; ++tt) {
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int hp = h == 0 ? 1 : (h == 1 ? 0 : h);
+        const int dz_lo = hp == 0 ? 0 : hp - 1;
+        const bool one = hp == 0 || hp == 3;
+        const uint32_t aoff = unit_off16(tt) + (uint32_t)(hp * HY * HX) + (uint32_t)(ks * 2 * (QUAD_BYTES / 16));
+        const uint64_t ad = ((uint64_t)a_hi << 32) | (a_lo + aoff);
+        const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo + tt * b_unit16 + ks * b_ks16 + dz_lo * ncol);
+        mma_tf32(dcol + (hp == 0 ? ncol : 0u), ad, bd, one ? idesc1 : idesc2, accf);
+        accf = 1u;
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -232,7 +268,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int ntaps = 27;
+  const int nunits = A.fold ? 9 : 27;
 
   if (warp == 3) {
     if (lane == 0) {  // ---------------- A producer: halo bricks, one TMA box per 32-channel chunk
@@ -262,12 +298,12 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
         int b, x0, y0, z0, n0, ks;
         decode_tile(A, tile, b, x0, y0, z0, n0, ks);
         for (int c = ks * A.cps; c < (ks + 1) * A.cps; ++c) {
-          // packed weights [chunk][tap][quad][cout][4]; a stage holds tps
-          // consecutive taps: one contiguous copy when the CTA owns every
-          // output channel, else one per (tap, quad)
-          const size_t tap_floats = (size_t)A.cqc * A.cout * 4;
-          const float* wc = A.w + (size_t)c * ntaps * tap_floats;
-          for (int t0 = 0; t0 < ntaps; t0 += A.tps) {
+          // packed weights [chunk][tap][quad][cout][4] (fold: [chunk][dydx][quad][dz][cout][4]);
+          // a stage holds tps consecutive units: one contiguous copy when the
+          // CTA owns every output channel, else one per (tap, quad)
+          const size_t tap_floats = (size_t)A.cqc * A.cout * 4 * (A.fold ? 3 : 1);
+          const float* wc = A.w + (size_t)c * nunits * tap_floats;
+          for (int t0 = 0; t0 < nunits; t0 += A.tps) {
             mbar_wait(&b_empty[bs], bp ^ 1);
             if (A.dbg & 8) {
               mbar_arrive(&b_full[bs]);
@@ -296,7 +332,8 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(A.ncol >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
       const uint32_t lbo_a = QUAD_BYTES, sbo_a = HX * 16;
-      const uint32_t lbo_b = A.ncol * 16, sbo_b = 128;
+      const uint32_t lbo_b = A.ncol * 16 * (A.fold ? 3 : 1), sbo_b = 128;
+      const uint32_t idesc2 = (idesc & ~(0x3Fu << 17)) | ((uint32_t)((2 * A.ncol) >> 3) << 17);
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
       int as = 0, ap = 0, bs = 0, bp = 0, li = 0;
       for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++li) {
@@ -309,18 +346,24 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           mbar_wait(&a_full[as], ap);
           fence_after();
           const uint32_t abase = a0 + as * A.a_bytes;
-          for (int t0 = 0; t0 < ntaps; t0 += A.tps) {
+          for (int t0 = 0; t0 < nunits; t0 += A.tps) {
             if (!A.resident || li == 0) {
               mbar_wait(&b_full[bs], bp);
               fence_after();
             }
-            const uint64_t ad0 = umma_desc(abase + tap_off16(t0) * 16u, lbo_a, sbo_a);
+            const uint64_t ad0 = umma_desc(abase + (A.fold ? unit_off16(t0) : tap_off16(t0)) * 16u, lbo_a, sbo_a);
             const uint64_t bd0 = umma_desc(b0 + bs * A.b_bytes, lbo_b, sbo_b);
             const uint32_t a_lo = (uint32_t)ad0, a_hi = (uint32_t)(ad0 >> 32);
             const uint32_t b_lo = (uint32_t)bd0, b_hi = (uint32_t)(bd0 >> 32);
-            const uint32_t b_tap16 = (uint32_t)(A.cqc * A.ncol);  // (cqc * ncol * 16 B) / 16
-            const uint32_t b_ks16 = (uint32_t)(2 * A.ncol);         // (2 * lbo_b) / 16
-            if (!(A.dbg & 2)) {
+            const uint32_t b_tap16 = (uint32_t)(A.cqc * A.ncol * (A.fold ? 3 : 1));  // one unit's weights / 16 B
+            const uint32_t b_ks16 = (uint32_t)(2 * A.ncol * (A.fold ? 3 : 1));         // (2 * lbo_b) / 16
+            if (!(A.dbg & 2) && A.fold) {
+              switch (A.tps) {
+                case 9: issue_stage_fold<9>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, idesc2, accf); break;
+                case 3: issue_stage_fold<3>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, idesc2, accf); break;
+                default: issue_stage_fold<1>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, idesc2, accf); break;
+              }
+            } else if (!(A.dbg & 2)) {
               switch (A.tps) {
                 case 27: issue_stage<27>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
                 case 9: issue_stage<9>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
@@ -356,6 +399,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
       const uint32_t dcol = tmem + lane_addr + (uint32_t)(buf * ZP * A.ncol);
       const int q0 = A.out_q0 + n0 / 4;
       const int gx = x0 + lx, gy = y0 + ly;
+      auto zcol = [&](int zp) { return (uint32_t)((A.fold ? ZP - 1 - zp : zp) * A.ncol); };
       if (A.ksplit > 1) {  // raw partial sums; conv_split_reduce_kernel finishes the layer
 #pragma unroll
         for (int zp = 0; zp < ZP; ++zp) {
@@ -363,7 +407,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           const bool ok = gx < S && gy < S && gz < S;
           for (int cg = 0; cg < A.ncol / 16; ++cg) {
             float v[16];
-            tmem_ld16(dcol + zp * A.ncol + cg * 16, v);
+            tmem_ld16(dcol + zcol(zp) + cg * 16, v);
             if (ok && !(A.dbg & 1)) {
 #pragma unroll
               for (int q = 0; q < 4; ++q)
@@ -382,8 +426,8 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           const int gz = z0 + zp;
           const bool ok = gx < S && gy < S && gz < S;
           float v[32];
-          tmem_ld16(dcol + zp * A.ncol, v);
-          tmem_ld16(dcol + zp * A.ncol + 16, v + 16);
+          tmem_ld16(dcol + zcol(zp), v);
+          tmem_ld16(dcol + zcol(zp) + 16, v + 16);
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             float m = v[i];
@@ -427,7 +471,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           const bool ok = gx < S && gy < S && gz < S;
           for (int cg = 0; cg < A.ncol / 16; ++cg) {
             float v[16];
-            tmem_ld16(dcol + zp * A.ncol + cg * 16, v);
+            tmem_ld16(dcol + zcol(zp) + cg * 16, v);
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               float m = v[i];
@@ -726,12 +770,14 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   A.a_bytes = (uint32_t)A.cqc * QUAD_BYTES;
   A.na = 2;
   const size_t budget = 227 * 1024 - 2048 - 1024;
-  const size_t tap_bytes = (size_t)A.cqc * A.ncol * 16;
+  A.fold = cout == 32 && A.nsplit == 1 && epi != EPI_POOL;
+  const int nunits = A.fold ? 9 : 27;
+  const size_t tap_bytes = (size_t)A.cqc * A.ncol * 16 * (A.fold ? 3 : 1);  // one weight unit
   A.resident = 0;
   int nbs = 0;
-  if (A.cps == 1 && A.ksplit == 1 && (size_t)A.na * A.a_bytes + 27 * tap_bytes <= budget) {
+  if (A.cps == 1 && A.ksplit == 1 && (size_t)A.na * A.a_bytes + nunits * tap_bytes <= budget) {
     A.resident = 1;  // e.g. enc1b: the 27-tap filter fits next to the halo double buffer
-    A.tps = 27;
+    A.tps = nunits;
     nbs = 1;
   } else {
     // as many taps per stage as leave >= 3 stages: each barrier handshake must
@@ -820,6 +866,9 @@ int tc_tconv(int nb, const float4* in, int in_cq, int cin, int cout, int Sin, in
   const size_t budget = 200 * 1024;
   int tg = 8;
   while (tg > 1 && ((size_t)T.a_bytes + (size_t)tg * cin * cout * 4 > budget || tg * cout > 256)) tg >>= 1;
+  // small grids: fewer taps per CTA (more CTAs, shorter serial MMA + epilogue chains)
+  const int64_t mt = (int64_t)ceil_div((int64_t)Sin * Sin * Sin, 128) * nb;
+  while (tg > 1 && mt * (8 / tg) < 2 * sm_count()) tg >>= 1;
   T.tg = tg;
   T.b_bytes = (uint32_t)(tg * cin * cout * 4);
   uint32_t cols = 32;

@@ -98,6 +98,12 @@ def _single_problem(C):
     return C
 
 
+def _row_stride(n3: int) -> int:
+    """Row stride of standalone (batch, n^3) device buffers: a multiple of 32
+    elements, as DeviceProblem.ld (the Krylov kernels load 16-byte pairs)."""
+    return (n3 + 31) // 32 * 32
+
+
 def apply_neural(params, r, dfield: DistanceField, smoothing=None, C=None, zero_distance: bool = False,
                  path: int = PATH_TCGEN05):
     """One preconditioner application z ~ C^-1 r (training.py:290-319)."""
@@ -110,7 +116,7 @@ def apply_neural(params, r, dfield: DistanceField, smoothing=None, C=None, zero_
     C = _single_problem(C)
     n = dfield.grid.n
     n3 = n ** 3
-    ld = C.prob.ld if C is not None else n3
+    ld = C.prob.ld if C is not None else _row_stride(n3)
     P = BatchedNeural(device_net(params, path), torch.as_tensor(dfield.values, device="cuda")[None], n, ld, 1,
                       C=C, smoothing=smoothing, zero_distance=zero_distance)
     V = torch.zeros((1, ld), dtype=torch.float64, device="cuda")
@@ -132,13 +138,15 @@ def apply_batched(params, residuals: list, dfields: list, path: int = PATH_TCGEN
     n = sizes.pop()
     n3 = n ** 3
     b = len(residuals)
-    R = torch.as_tensor(np.stack([np.asarray(r, dtype=float) for r in residuals]), device="cuda")
+    ld = _row_stride(n3)
+    R = torch.zeros((b, ld), dtype=torch.float64, device="cuda")
+    R[:, :n3] = torch.as_tensor(np.stack([np.asarray(r, dtype=float) for r in residuals]), device="cuda")
     D = torch.as_tensor(np.stack([d.values for d in dfields]), device="cuda")
-    P = BatchedNeural(device_net(params, path), D, n, n3, b)
+    P = BatchedNeural(device_net(params, path), D, n, ld, b)
     Z = torch.zeros_like(R)
     sel = torch.arange(b, dtype=torch.int32, device="cuda")
     P.apply_device(R, Z, sel, list(range(b)))
-    Zh = Z.cpu().numpy()
+    Zh = Z[:, :n3].cpu().numpy()
     return [Zh[i].copy() for i in range(b)]
 
 
@@ -154,7 +162,7 @@ class NeuralPreconditioner(Preconditioner):
         self.C = _single_problem(C)
         self.zero_distance = zero_distance
         n = dfield.grid.n
-        ld = self.C.prob.ld if self.C is not None else n ** 3
+        ld = self.C.prob.ld if self.C is not None else _row_stride(n ** 3)
         if smoothing is not None and self.C is None:
             raise ValueError("smoothing needs the reduced operator")
         self._dev = BatchedNeural(device_net(params, path), torch.as_tensor(dfield.values, device="cuda")[None],

@@ -1,0 +1,12 @@
+cd $GRAFT_REPO_ROOT
+export PYTHONDONTWRITEBYTECODE=1
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | grep -E "^FAILED|passed|failed|Error|assert" | head -30 > gpurun_out/t_t.log
+timeout 600 python tools/step_breakdown.py --maxit 60 --out gpurun_out/breakdown_t.json > gpurun_out/breakdown_t.log 2>&1
+timeout 600 python bench.py --steps 3 --warmup 3 --maxit 300 --no-cpu-baseline > gpurun_out/bench_t.log 2>&1
+cat gpurun_out/t_t.log; head -24 gpurun_out/breakdown_t.log; python - <<'PY'
+import json
+d=json.loads(open('gpurun_out/bench_t.log').read().strip().splitlines()[-1])
+print(d['value'], d['ms_per_step'], d['e2e'])
+print({k:(round(v['ms']*1e3,1), round(v['tflops'],1)) for k,v in d['conv_layers'].items()})
+print(json.dumps(d.get('target_128'))[:1200])
+PY
