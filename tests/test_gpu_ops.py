@@ -62,7 +62,8 @@ def test_ilu_sweeps_bitwise(gpu, name):
     assert np.array_equal(z, g["ilu_z"])
 
 
-@pytest.mark.parametrize("bc3d,nc,n", [("neumann", 1, 65), ("dirichlet", 8, 65), ("dirichlet", 8, 33)])
+@pytest.mark.parametrize("bc3d,nc,n", [("neumann", 1, 65), ("dirichlet", 8, 65), ("dirichlet", 8, 33),
+                                       ("dirichlet", 8, 97), ("neumann", 8, 50)])
 def test_spmv_large_vs_oracle(gpu, bc3d, nc, n):
     from paper_2505_08491_b200 import assembly as A, geometry as G
     from oracle import problem as OP
@@ -78,11 +79,73 @@ def test_spmv_large_vs_oracle(gpu, bc3d, nc, n):
     assert rel(A.reduced_operator(s) @ x[:s.n3], OP.reduced_operator(o) @ x[:s.n3]) <= 1e-10
 
 
-def test_batched_spmv_equals_serial_bitwise(gpu):
+def _kron_k00(x3, n, h, kO, sO):
+    """K00 x (Neumann) by sum factorisation of the 1D P1 stiffness / mass (assembly.py:83-125)."""
+    def tri(v, axis, d_in, d_end, off):
+        v = np.moveaxis(v, axis, -1)
+        out = d_in * v
+        out[..., 0] = d_end * v[..., 0]
+        out[..., -1] = d_end * v[..., -1]
+        out[..., 1:] += off * v[..., :-1]
+        out[..., :-1] += off * v[..., 1:]
+        return np.moveaxis(out, -1, axis)
+    K = lambda v, a: tri(v, a, 2.0 / h, 1.0 / h, -1.0 / h)  # noqa: E731
+    M = lambda v, a: tri(v, a, 4.0 * h / 6.0, 2.0 * h / 6.0, h / 6.0)  # noqa: E731
+    v = x3.reshape(n, n, n)  # [z][y][x]
+    out = kO * (M(M(K(v, 2), 1), 0) + M(K(M(v, 2), 1), 0) + K(M(M(v, 2), 1), 0)) + sO * M(M(M(v, 2), 1), 0)
+    return out.ravel()
+
+
+@pytest.mark.parametrize("n", [270, 130])
+def test_stencil_multi_tile_vs_kronecker(gpu, n):
+    """Grids wider than one x-tile (256 columns) and odd/even row pitches."""
+    import torch
+    from paper_2505_08491_b200 import assembly as A, geometry as G
+    from paper_2505_08491_b200.operators import CouplingOps
+    s = A.assemble_coupled_system(G.StructuredGrid(n), G.random_tree(2, 5, 0.01), A.PhysicalParams(epsilon=0.01),
+                                  elems_per_edge=2)
+    pb = A.DeviceProblem([s])
+    x = np.random.default_rng(n).standard_normal(s.n3)
+    X, Y = pb.zeros(), pb.zeros()
+    X[0, :s.n3] = torch.as_tensor(x, device="cuda")
+    CouplingOps(pb).stencil(X, Y)
+    want = _kron_k00(x, n, 1.0 / (n - 1), s.params.k_omega, s.params.sigma_omega)
+    assert rel(Y[0, :s.n3].cpu().numpy(), want) <= 1e-12
+
+
+@pytest.mark.parametrize("n,bc3d", [(65, "dirichlet"), (65, "neumann"), (17, "dirichlet")])
+def test_jacobi_sweep_vs_oracle(gpu, n, bc3d):
+    """Fused Jacobi epilogue x + omega (r - C x) / diag(C) (krylov.py:290-299) on both stencil kernels."""
+    import torch
+    from paper_2505_08491_b200 import assembly as A, geometry as G
+    from paper_2505_08491_b200.operators import ReducedOperator
+    from oracle import problem as OP
+    R = 0.01
+    s = A.assemble_coupled_system(G.StructuredGrid(n), G.random_tree(16, 77, R), A.PhysicalParams(epsilon=R),
+                                  n_circle=8, elems_per_edge=8, bc3d=bc3d, f1d=1.0)
+    o = OP.assemble_coupled_system(OP.StructuredGrid(n), OP.random_tree(16, 77, R), OP.PhysicalParams(epsilon=R),
+                                   n_circle=8, elems_per_edge=8, bc3d=bc3d, f1d=1.0)
+    C = OP.reduced_operator(o).tocsr()
+    rng = np.random.default_rng(n)
+    x, r = rng.standard_normal(s.n3), rng.standard_normal(s.n3)
+    want = x + (2.0 / 3.0) * (r - C @ x) / C.diagonal()
+    pb = A.DeviceProblem([s])
+    op = ReducedOperator(pb)
+    X, Rr, Xo, T = pb.zeros(), pb.zeros(), pb.zeros(), pb.zeros()
+    X[0, :s.n3] = torch.as_tensor(x, device="cuda")
+    Rr[0, :s.n3] = torch.as_tensor(r, device="cuda")
+    op.jacobi(Rr, X, Xo, 2.0 / 3.0, T)
+    assert rel(Xo[0, :s.n3].cpu().numpy(), want) <= 1e-10
+    op.jacobi(Rr, None, Xo, 2.0 / 3.0, T)  # zero initial guess
+    assert rel(Xo[0, :s.n3].cpu().numpy(), (2.0 / 3.0) * r / C.diagonal()) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [33, 65])
+def test_batched_spmv_equals_serial_bitwise(gpu, n):
     import torch
     from paper_2505_08491_b200 import assembly as A, geometry as G
     from paper_2505_08491_b200.operators import CoupledOperator
-    grid = G.StructuredGrid(33)
+    grid = G.StructuredGrid(n)
     systems = [A.assemble_coupled_system(grid, G.random_tree(8 + 4 * i, 10 + i, 0.015),
                                          A.PhysicalParams(epsilon=0.015, beta=0.5 + i), elems_per_edge=16)
                for i in range(3)]
