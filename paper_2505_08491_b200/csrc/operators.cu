@@ -263,9 +263,20 @@ __global__ void __launch_bounds__(256) stencil_bulk_kernel(const mdp_problem P, 
   __syncthreads();
   // element offset of column cl inside a staged row (0 or 1: the copy starts at an even element)
   auto row_off = [&](int kk, int jj) { return (int)(((int64_t)kk * nn + (int64_t)jj * n + cl) & 1); };
+  // whole-row tiles: the CTA's rows jlo..jhi of a plane are one contiguous run -> one copy per plane
+  const bool whole = xtiles == 1;
+  const int jlo = max(j0 - 1, 0), jhi = min(j0 + RY, n - 1);
   auto issue = [&](int kk, int slot) {
     if (!line_ok(kk)) {
       mbar_arrive(&full[slot]);
+      return;
+    }
+    if (whole) {
+      const int64_t e0 = (int64_t)kk * nn + (int64_t)jlo * n;
+      const int64_t a0 = e0 & ~(int64_t)1;
+      const uint32_t b = (uint32_t)(((e0 + (int64_t)(jhi - jlo + 1) * n - a0 + 1) & ~(int64_t)1) * 8);
+      mbar_expect_tx(&full[slot], b);
+      bulk_load(ring + (size_t)slot * NR * rowlen, xp + a0, b, &full[slot]);
       return;
     }
     uint32_t bytes = 0;
@@ -315,7 +326,9 @@ __global__ void __launch_bounds__(256) stencil_bulk_kernel(const mdp_problem P, 
     for (int a = 0; a < NR; ++a) {
       double v = 0.0, l = 0.0, r = 0.0;
       if (pok && rowv[a]) {
-        const double* row = S + a * rowlen + row_off(kk, j0 - 1 + a) + (i - cl);
+        const double* row =
+            whole ? S + (int)((((int64_t)kk * nn + (int64_t)jlo * n) & 1)) + (int64_t)(j0 - 1 + a - jlo) * n + i
+                  : S + a * rowlen + row_off(kk, j0 - 1 + a) + (i - cl);
         if (okc) v = row[0];
         if (okl) l = row[-1];
         if (okr) r = row[1];

@@ -102,7 +102,7 @@ def test_stencil_multi_tile_vs_kronecker(gpu, n):
     import torch
     from paper_2505_08491_b200 import assembly as A, geometry as G
     from paper_2505_08491_b200.operators import CouplingOps
-    s = A.assemble_coupled_system(G.StructuredGrid(n), G.random_tree(2, 5, 0.01), A.PhysicalParams(epsilon=0.01),
+    s = A.assemble_coupled_system(G.StructuredGrid(n), G.random_tree(2, 5, 1e-3), A.PhysicalParams(epsilon=1e-3),
                                   elems_per_edge=2)
     pb = A.DeviceProblem([s])
     x = np.random.default_rng(n).standard_normal(s.n3)
