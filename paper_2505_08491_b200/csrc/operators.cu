@@ -13,7 +13,6 @@
 // which equals full_operator(s) @ x.
 #include <stdlib.h>
 
-#include "async.cuh"
 #include "common.cuh"
 
 namespace mdp {
@@ -89,6 +88,10 @@ __device__ double g_zero_row[32];  // zero page: out-of-domain rows read from he
 // page through a pointer that does not advance.  Optional fused Jacobi
 // epilogue out = xin + omega (r - y) / diag(C) (coupling correction follows
 // in the pull).
+#ifndef STENCIL_PF
+#define STENCIL_PF 2  // planes of loads in flight per warp (tools/stencil_sweep.py A/B)
+#endif
+
 struct GatherArgs {  // optional Pi gather folded into the stencil launch (last y-slice)
   const double* x3;
   const double* x1;
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(128) stencil_kernel(const mdp_problem P, const
                                                        double* __restrict__ y, int64_t ldy, int zchunk,
                                                        const double* __restrict__ jr, double omega,
                                                        const GatherArgs G) {
-  constexpr int RY = 2, NR = RY + 2;
+  constexpr int RY = 2, NR = RY + 2, PF = STENCIL_PF;
   const int n = P.n;
   const int s = sys_of(sel, blockIdx.z);
   if (GATHER && blockIdx.y == gridDim.y - 1) {  // independent of the stencil: runs alongside it
@@ -161,14 +164,17 @@ __global__ void __launch_bounds__(128) stencil_kernel(const mdp_problem P, const
   double* yrow = yp + (int64_t)z0 * nn + (int64_t)j * n + i;  // output (z0, j, i)
   const double* xrow = xp + (int64_t)z0 * nn + (int64_t)j * n + i;
   int64_t goff = (int64_t)s * ldy + (int64_t)z0 * nn + (int64_t)j * n + i;
-  double cur[NR], nx1[NR], nx2[NR];
-  load(z0 - 1, cur);
-  load(z0, nx1);
+  // register ring: q[0] = plane kk, q[1..PF] = the next PF planes (loads in flight)
+  double q[PF + 1][NR];
+#pragma unroll
+  for (int p = 0; p < PF; ++p)
+    if (z0 - 1 + p <= z1) load(z0 - 1 + p, q[p]);
+  double* cur = q[0];
   double Pm[RY], P0[RY], Rm[RY], R0[RY];
 #pragma unroll
   for (int r = 0; r < RY; ++r) Pm[r] = P0[r] = Rm[r] = R0[r] = 0.0;
   for (int kk = z0 - 1; kk <= z1; ++kk) {
-    if (kk + 2 <= z1) load(kk + 2, nx2);
+    if (kk + PF <= z1) load(kk + PF, q[PF]);
     double kx[NR], mx[NR];
 #pragma unroll
     for (int a = 0; a < NR; ++a) {
@@ -203,173 +209,9 @@ __global__ void __launch_bounds__(128) stencil_kernel(const mdp_problem P, const
       goff += nn;
     }
 #pragma unroll
-    for (int a = 0; a < NR; ++a) {
-      cur[a] = nx1[a];
-      nx1[a] = nx2[a];
-    }
-  }
-}
-
-// Bulk-copy ring variant of the stencil (large grids).  CTA = an x-tile of
-// XT columns (one thread per column) x RY rows, marching z over [z0, z1).
-// One elected thread streams each z-plane's RY+2 row segments (columns
-// x0-1 .. x0+XT, widened to 16-byte-aligned element pairs) into an NS-deep
-// shared-memory ring with cp.async.bulk + mbarrier transaction counts, so
-// ~NS-1 planes per CTA are in flight without holding registers; every
-// thread reads its column and both x-neighbours from shared memory.  Rows /
-// planes outside the domain or on eliminated (Dirichlet) cube nodes are not
-// copied and read as zero.  Arithmetic per output is that of stencil_kernel.
-constexpr int BULK_NS = 4;
-
-template <bool JAC, bool GATHER, int RY>
-__global__ void __launch_bounds__(256) stencil_bulk_kernel(const mdp_problem P, const int32_t* sel,
-                                                            const double* __restrict__ x, int64_t ldx,
-                                                            double* __restrict__ y, int64_t ldy, int zchunk,
-                                                            int xtiles, int ytiles,
-                                                            const double* __restrict__ jr, double omega,
-                                                            const GatherArgs G) {
-  using namespace ::mdp::async;
-  constexpr int NR = RY + 2, NS = BULK_NS;
-  extern __shared__ __align__(16) double ring[];
-  const int n = P.n;
-  const int s = sys_of(sel, blockIdx.z);
-  if (GATHER && blockIdx.y == gridDim.y - 1) {
-    gather_rows(P, s, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5), G.x3, G.x1,
-                ldx, G.s_out);
-    return;
-  }
-  if ((int)blockIdx.x >= xtiles * ytiles) return;
-  const int XT = blockDim.x, rowlen = XT + 4;
-  uint64_t* full = (uint64_t*)(ring + (size_t)NS * NR * rowlen);
-  uint64_t* empty = full + NS;
-  const int x0 = (blockIdx.x % xtiles) * XT, j0 = (blockIdx.x / xtiles) * RY;
-  const int z0 = blockIdx.y * zchunk, z1 = min(n, z0 + zchunk);
-  if (z0 >= n) return;
-  const int tid = threadIdx.x, lane = tid & 31, nwarps = blockDim.x >> 5;
-  const int i = x0 + tid;
-  const bool dir = P.bc3d != 0;
-  const double* xp = x + (int64_t)s * ldx;
-  double* yp = y + (int64_t)s * ldy;
-  const int64_t nn = (int64_t)n * n;
-  const int cl = max(x0 - 1, 0), ch = min(x0 + XT, n - 1);  // columns staged per row (inclusive)
-  auto line_ok = [&](int t) { return t >= 0 && t < n && !(dir && (t == 0 || t == n - 1)); };
-  if (tid == 0) {
-    for (int k = 0; k < NS; ++k) {
-      mbar_init(&full[k], 1);
-      mbar_init(&empty[k], nwarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  // element offset of column cl inside a staged row (0 or 1: the copy starts at an even element)
-  auto row_off = [&](int kk, int jj) { return (int)(((int64_t)kk * nn + (int64_t)jj * n + cl) & 1); };
-  // whole-row tiles: the CTA's rows jlo..jhi of a plane are one contiguous run -> one copy per plane
-  const bool whole = xtiles == 1;
-  const int jlo = max(j0 - 1, 0), jhi = min(j0 + RY, n - 1);
-  auto issue = [&](int kk, int slot) {
-    if (!line_ok(kk)) {
-      mbar_arrive(&full[slot]);
-      return;
-    }
-    if (whole) {
-      const int64_t e0 = (int64_t)kk * nn + (int64_t)jlo * n;
-      const int64_t a0 = e0 & ~(int64_t)1;
-      const uint32_t b = (uint32_t)(((e0 + (int64_t)(jhi - jlo + 1) * n - a0 + 1) & ~(int64_t)1) * 8);
-      mbar_expect_tx(&full[slot], b);
-      bulk_load(ring + (size_t)slot * NR * rowlen, xp + a0, b, &full[slot]);
-      return;
-    }
-    uint32_t bytes = 0;
+    for (int p = 0; p < PF; ++p)
 #pragma unroll
-    for (int a = 0; a < NR; ++a) {
-      const int jj = j0 - 1 + a;
-      if (!line_ok(jj)) continue;
-      const int64_t e0 = (int64_t)kk * nn + (int64_t)jj * n + cl;
-      const int64_t a0 = e0 & ~(int64_t)1;
-      bytes += (uint32_t)(((e0 + (ch - cl) - a0 + 2) & ~(int64_t)1) * 8);
-    }
-    mbar_expect_tx(&full[slot], bytes);
-    double* dst = ring + (size_t)slot * NR * rowlen;
-#pragma unroll
-    for (int a = 0; a < NR; ++a) {
-      const int jj = j0 - 1 + a;
-      if (!line_ok(jj)) continue;
-      const int64_t e0 = (int64_t)kk * nn + (int64_t)jj * n + cl;
-      const int64_t a0 = e0 & ~(int64_t)1;
-      const uint32_t b = (uint32_t)(((e0 + (ch - cl) - a0 + 2) & ~(int64_t)1) * 8);
-      bulk_load(dst + a * rowlen, xp + a0, b, &full[slot]);
-    }
-  };
-  const int np = (z1 - z0) + 2;  // planes z0-1 .. z1
-  if (tid == 0)
-    for (int p = 0; p < NS - 1 && p < np; ++p) issue(z0 - 1 + p, p);
-
-  const Line1D c = make_line(P.h);
-  const double kO = P.k_omega, sO = P.sigma_omega;
-  const bool col_in = i < n;
-  const int ic = col_in ? i : n - 1;
-  const double kdx = kdiag(c, ic, n), mdx = mdiag(c, ic, n);
-  const bool okc = col_in && line_ok(i), okl = col_in && line_ok(i - 1), okr = col_in && line_ok(i + 1);
-  bool rowv[NR];
-#pragma unroll
-  for (int a = 0; a < NR; ++a) rowv[a] = line_ok(j0 - 1 + a);
-  double Pm[RY], P0[RY], Rm[RY], R0[RY];
-#pragma unroll
-  for (int r = 0; r < RY; ++r) Pm[r] = P0[r] = Rm[r] = R0[r] = 0.0;
-  for (int p = 0; p < np; ++p) {
-    const int kk = z0 - 1 + p, slot = p % NS;
-    mbar_wait(&full[slot], (uint32_t)((p / NS) & 1));
-    const double* S = ring + (size_t)slot * NR * rowlen;
-    const bool pok = line_ok(kk);
-    double kx[NR], mx[NR];
-#pragma unroll
-    for (int a = 0; a < NR; ++a) {
-      double v = 0.0, l = 0.0, r = 0.0;
-      if (pok && rowv[a]) {
-        const double* row =
-            whole ? S + (int)((((int64_t)kk * nn + (int64_t)jlo * n) & 1)) + (int64_t)(j0 - 1 + a - jlo) * n + i
-                  : S + a * rowlen + row_off(kk, j0 - 1 + a) + (i - cl);
-        if (okc) v = row[0];
-        if (okl) l = row[-1];
-        if (okr) r = row[1];
-      }
-      const double lr = l + r;
-      kx[a] = c.ko * lr + kdx * v;
-      mx[a] = c.mo * lr + mdx * v;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[slot]);
-    if (tid == 0 && p + NS - 1 < np) {
-      const int q = p + NS - 1, sl = q % NS;
-      if (q >= NS) mbar_wait(&empty[sl], (uint32_t)(((q / NS) - 1) & 1));
-      issue(z0 - 1 + q, sl);
-    }
-    const int ko = kk - 1;
-    const bool emit = ko >= z0;
-    const double kd = kdiag(c, ko < 0 ? 0 : ko, n), md = mdiag(c, ko < 0 ? 0 : ko, n);
-    const bool planeb = dir && (ko == 0 || ko == n - 1);
-#pragma unroll
-    for (int r = 0; r < RY; ++r) {
-      const int jrow = j0 + r;
-      const int jc = jrow < n ? jrow : n - 1;
-      const double kdy = kdiag(c, jc, n), mdy = mdiag(c, jc, n);
-      const double msum = mx[r] + mx[r + 2];
-      const double c1 = c.mo * (kx[r] + kx[r + 2]) + mdy * kx[r + 1];
-      const double c2 = c.ko * msum + kdy * mx[r + 1];
-      const double c3 = c.mo * msum + mdy * mx[r + 1];
-      const double Pn = kO * (c1 + c2) + sO * c3;
-      const double Rn = kO * c3;
-      if (emit && col_in && jrow < n) {
-        const int64_t g = (int64_t)ko * nn + (int64_t)jrow * n + i;
-        double out = c.mo * (Pm[r] + Pn) + md * P0[r] + c.ko * (Rm[r] + Rn) + kd * R0[r];
-        const bool colb = dir && (i == 0 || i == n - 1 || jrow == 0 || jrow == n - 1);
-        if (colb || planeb) out = xp[g];
-        if (JAC) out = xp[g] + (omega * (jr[(int64_t)s * ldy + g] - out)) / P.diag_c[(int64_t)s * ldy + g];
-        yp[g] = out;
-      }
-      Pm[r] = P0[r]; P0[r] = Pn;
-      Rm[r] = R0[r]; R0[r] = Rn;
-    }
+      for (int a = 0; a < NR; ++a) q[p][a] = q[p + 1][a];
   }
 }
 
@@ -504,67 +346,10 @@ __global__ void __launch_bounds__(256) distance_kernel(int n, const double* __re
   if (v < n3) out[v] = best;
 }
 
-#ifndef STENCIL_BULK_MIN_N
-#define STENCIL_BULK_MIN_N 48  // grids from this size use the bulk-copy ring kernel
-#endif
-#ifndef STENCIL_RY
-#define STENCIL_RY 8
-#endif
-
-template <int RY>
-static int launch_stencil_bulk(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* x,
-                               int64_t ldx, double* y, int64_t ldy, cudaStream_t st, const double* jr,
-                               double omega, const GatherArgs* g) {
-  const int n = p->n;
-  int XT = ((n + 31) / 32) * 32;
-  XT = XT > 256 ? 256 : XT;
-  const int xtiles = ceil_div(n, XT), ytiles = ceil_div(n, RY);
-  const int tiles = xtiles * ytiles;
-  // a few CTAs per SM, each marching a long z-chunk (the ring keeps its loads in flight)
-  int zch = ceil_div((int64_t)3 * sm_count(), (int64_t)tiles * nsel);
-  const int zmax = n / 8 > 1 ? n / 8 : 1;
-  zch = zch < 1 ? 1 : (zch > zmax ? zmax : zch);
-  int zchunk = ceil_div(n, zch);
-  {
-    static int forced = -1;  // MDP_STENCIL_ZCHUNK: tuning experiments only (tools/stencil_sweep.py)
-    if (forced < 0) {
-      const char* e = getenv("MDP_STENCIL_ZCHUNK");
-      forced = e ? atoi(e) : 0;
-    }
-    if (forced > 0) zchunk = forced < n ? forced : n;
-  }
-  zch = ceil_div(n, zchunk);
-  const bool gat = g != nullptr && p->qmax > 0;
-  int bx = tiles;
-  if (gat) bx = bx > ceil_div(p->qmax, XT / 32) ? bx : ceil_div(p->qmax, XT / 32);
-  dim3 grid(bx, zch + (gat ? 1 : 0), nsel);
-  const size_t smem = (size_t)BULK_NS * (RY + 2) * (XT + 4) * sizeof(double) + 2 * BULK_NS * sizeof(uint64_t);
-  GatherArgs G = gat ? *g : GatherArgs{nullptr, nullptr, nullptr};
-#define MDP_BULK(J, GA)                                                                                          \
-  do {                                                                                                           \
-    static bool attr = false;                                                                                    \
-    if (!attr) {                                                                                                 \
-      cudaFuncSetAttribute(stencil_bulk_kernel<J, GA, RY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-      attr = true;                                                                                               \
-    }                                                                                                            \
-    stencil_bulk_kernel<J, GA, RY><<<grid, XT, smem, st>>>(*p, sel, x, ldx, y, ldy, zchunk, xtiles, ytiles, jr, omega, G); \
-  } while (0)
-  if (jr) {
-    if (gat) MDP_BULK(true, true); else MDP_BULK(true, false);
-  } else {
-    if (gat) MDP_BULK(false, true); else MDP_BULK(false, false);
-  }
-#undef MDP_BULK
-  MDP_LAUNCH_CHECK("stencil_bulk_kernel");
-  return MDP_OK;
-}
-
 static int launch_stencil(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* x,
                           int64_t ldx, double* y, int64_t ldy, cudaStream_t st, const double* jr = nullptr,
                           double omega = 0.0, const GatherArgs* g = nullptr) {
   const int n = p->n;
-  if (n >= STENCIL_BULK_MIN_N)
-    return launch_stencil_bulk<STENCIL_RY>(p, nsel, sel, x, ldx, y, ldy, st, jr, omega, g);
   const int64_t warps = (int64_t)ceil_div(n, 30) * ceil_div(n, 2);  // (x-tile, row pair) per plane
   int bx = ceil_div(warps, 4);
   // z-chunks: enough warps to fill the machine; chunks of >= 16 planes when the
