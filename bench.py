@@ -180,7 +180,7 @@ def conv_layer_times(n, reps=20):
                             device="cuda")
         So = S // 2 if pool else S
         Y = torch.empty(cout * So ** 3, dtype=torch.float32, device="cuda")
-        scr = torch.empty(max(lib.mdp_conv3_scratch_bytes(1, S, cin, cout), 16), dtype=torch.uint8, device="cuda")
+        scr = torch.zeros(max(lib.mdp_conv3_scratch_bytes(1, S, cin, cout), 16), dtype=torch.uint8, device="cuda")
         st = _ext.stream()
 
         def run():

@@ -213,6 +213,9 @@ typedef struct mdp_unet {
   int32_t path;     /* 0: tcgen05 TF32 implicit GEMM, 1: CUDA-core FP32 check path */
   const float* w[11];  /* packed weights, ARCHITECTURE order */
   const float* b[11];  /* biases (NULL where the layer has none)           */
+  int32_t accumulate;  /* 1: z_s += scale_i * U(..) (fused z + z_net of the
+                          smoothed apply, training.py:305-311); 0: z_s = ...  */
+  int32_t reserved;
 } mdp_unet;
 
 size_t mdp_unet_workspace_bytes(int32_t n, int32_t nb, int32_t path);
@@ -231,7 +234,9 @@ int mdp_conv3_layer(int32_t path, int32_t nb, int32_t S, int32_t cin, int32_t co
                     const float* in, int32_t in_cq, int32_t in_q0, const float* w, const float* bias,
                     int32_t relu, float* out, int32_t out_cq, int32_t out_q0, int32_t pool,
                     void* scratch, size_t scratch_bytes, void* stream);
-/* Scratch bytes mdp_conv3_layer (path 0) needs for split-K partial sums. */
+/* Scratch bytes mdp_conv3_layer (path 0) needs for split-K partial sums and
+ * arrival tickets.  The scratch must be zero-initialised before its first
+ * use; every call leaves the ticket area zero again. */
 size_t mdp_conv3_scratch_bytes(int32_t nb, int32_t S, int32_t cin, int32_t cout);
 
 /* ------------------------------------------------------------------ */

@@ -39,7 +39,8 @@ class MdpIlu(C.Structure):
 
 
 class MdpUnet(C.Structure):
-    _fields_ = [("n", _i32), ("path", _i32), ("w", _vp * 11), ("b", _vp * 11)]
+    _fields_ = [("n", _i32), ("path", _i32), ("w", _vp * 11), ("b", _vp * 11), ("accumulate", _i32),
+                ("reserved", _i32)]
 
 
 _SIGS = {

@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(128) head_kernel(const float4* __restrict__ d1
                                                     const float* __restrict__ w1, const float* __restrict__ b1,
                                                     const float* __restrict__ w2, const float* __restrict__ b2,
                                                     const int32_t* sel, const double* __restrict__ rnorm,
-                                                    double* __restrict__ z, int64_t ldz) {
+                                                    double* __restrict__ z, int64_t ldz, int accumulate) {
   __shared__ float ws[16 * 32 + 16 + 16 + 1];
   for (int t = threadIdx.x; t < 512; t += blockDim.x) ws[t] = w1[t];
   for (int t = threadIdx.x; t < 16; t += blockDim.x) {
@@ -240,8 +240,8 @@ __global__ void __launch_bounds__(128) head_kernel(const float4* __restrict__ d1
     d[4 * q] = a.x; d[4 * q + 1] = a.y; d[4 * q + 2] = a.z; d[4 * q + 3] = a.w;
   }
   const float y = head_eval(d, ws, ws + 512, ws + 528, ws + 544);
-  const int s = sys_of(sel, b);
-  z[s * ldz + v] = rnorm[b] * (double)y;
+  double* zp = z + sys_of(sel, b) * ldz + v;
+  *zp = accumulate ? *zp + rnorm[b] * (double)y : rnorm[b] * (double)y;
 }
 
 // ---------------------------------------------------------------------------
@@ -321,12 +321,17 @@ UnetPlan unet_plan(int n, int nb, int path) {
     p.o_scr = p.scr_bytes = 0;
   } else {
     p.o_d1 = p.o_e2 = p.o_e3 = 0;
-    size_t scr = 0;
+    // layers share one scratch: room for the largest partial-sum set plus the
+    // largest ticket set (tickets live at the end of the scratch)
+    size_t part = 0, tick = 0;
     const int shp[6][3] = {{n, 16, 32}, {n, 32, 64}, {p.m, 64, 128}, {p.q, 128, 128}, {p.m, 128, 64}, {n, 64, 32}};
     for (auto& L : shp) {
-      size_t b = tc_conv3_scratch_bytes(nb, L[0], L[1], L[2]);
-      scr = b > scr ? b : scr;
+      const size_t t = tc_conv3_ticket_bytes(nb, L[0], L[1], L[2]);
+      const size_t pb = tc_conv3_scratch_bytes(nb, L[0], L[1], L[2]) - t;
+      part = pb > part ? pb : part;
+      tick = t > tick ? t : tick;
     }
+    const size_t scr = part + tick;
     p.scr_bytes = scr;
     p.o_scr = scr ? take(scr) : 0;
   }
@@ -422,12 +427,12 @@ extern "C" int mdp_unet_apply(const mdp_unet* net, int32_t nb, const int32_t* se
       return rc;
     if ((rc = tc_tconv(nb, d2, 16, 64, 32, m, op1, net->w[7], net->b[7], c1, 16, 0, st))) return rc;
     // dec1 with head1 -> head2 -> ||r|| scaling fused into its epilogue
-    HeadArgs H{net->w[9], net->b[9], net->w[10], net->b[10], sel, rnorm, z, ldz};
+    HeadArgs H{net->w[9], net->b[9], net->w[10], net->b[10], sel, rnorm, z, ldz, net->accumulate};
     return tc_conv3(nb, n, 64, 32, c1, 16, 0, net->w[8], net->b[8], 1, nullptr, 0, 0, EPI_HEAD, &H, ws + P.o_scr,
                     P.scr_bytes, st);
   }
   head_kernel<<<dim3(ceil_div(N, 128), nb), 128, 0, st>>>(d1, n, net->w[9], net->b[9], net->w[10], net->b[10],
-                                                          sel, rnorm, z, ldz);
+                                                          sel, rnorm, z, ldz, net->accumulate);
   MDP_LAUNCH_CHECK("head_kernel");
   return MDP_OK;
 }

@@ -231,16 +231,19 @@ class DeviceUNet:
         if self._ws is None or self._ws.numel() < nbytes:
             if self._ws is not None:
                 self._old.append(self._ws)
-            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._ws = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
         return self._ws
 
-    def apply(self, n: int, R, ld: int, rnorm, D, ldd: int, Z, ldz: int, sel=None, nb=None):
-        """Z_s = rnorm_i * U([R_s / rnorm_i | D_s]) for the selected systems."""
+    def apply(self, n: int, R, ld: int, rnorm, D, ldd: int, Z, ldz: int, sel=None, nb=None,
+              accumulate: bool = False):
+        """Z_s = rnorm_i * U([R_s / rnorm_i | D_s]) for the selected systems
+        (Z_s += ... with accumulate)."""
         nb = int(sel.numel()) if sel is not None else int(nb)
         if n < MIN_INPUT_SIZE:
             raise ValueError(f"spatial size must be at least {MIN_INPUT_SIZE}")
         ws = self.workspace(n, nb)
         self.desc.n = n
+        self.desc.accumulate = int(accumulate)
         _ext.check(self.lib.mdp_unet_apply(self.desc, nb, None if sel is None else sel.data_ptr(),
                                            R.data_ptr(), ld, rnorm.data_ptr(), D.data_ptr(), ldd, Z.data_ptr(),
                                            ldz, ws.data_ptr(), ws.numel(), _ext.stream()))

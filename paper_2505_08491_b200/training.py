@@ -45,7 +45,6 @@ class BatchedNeural:
             self.t1 = torch.zeros((nsys, ld), **f)
             self.t2 = torch.zeros((nsys, ld), **f)
             self.rr = torch.zeros((nsys, ld), **f)
-            self.zn = torch.zeros((nsys, ld), **f)
             self.tmp = torch.zeros((nsys, ld), **f)
         self.lib = _ext.lib()
 
@@ -77,10 +76,8 @@ class BatchedNeural:
         _ext.check(self.lib.mdp_residual(m, sel.data_ptr(), V.data_ptr(), self.tmp.data_ptr(), self.rr.data_ptr(),
                                          self.ld, self.n3, self.rn.data_ptr(), self.work.data_ptr(),
                                          _ext.stream()))
-        self.net.apply(self.n, self.rr, self.ld, self.rn, self.D, self.n3, self.zn, self.ld, sel=sel)
-        # z = z + zn, then maxit post sweeps from z
-        _ext.check(self.lib.mdp_axpby(m, sel.data_ptr(), 1.0, self.zn.data_ptr(), 1.0, cur.data_ptr(), self.ld,
-                                      self.n3, _ext.stream()))
+        # z = z + U(rr) (accumulated by the fused head epilogue), then maxit post sweeps from z
+        self.net.apply(self.n, self.rr, self.ld, self.rn, self.D, self.n3, cur, self.ld, sel=sel, accumulate=True)
         src = cur
         for it in range(maxit):
             out = Z if it == maxit - 1 else (self.t2 if src is self.t1 else self.t1)

@@ -11,7 +11,7 @@ X = torch.as_tensor(rng.standard_normal(cin * S ** 3).astype(np.float32), device
 W = torch.as_tensor(neural.pack_conv(rng.standard_normal((cout, cin, 3, 3, 3)) * 0.05, 0).ravel(), device="cuda")
 So = S // 2 if pool else S
 Y = torch.empty(cout * So ** 3, dtype=torch.float32, device="cuda")
-scr = torch.empty(max(lib.mdp_conv3_scratch_bytes(1, S, cin, cout), 16), dtype=torch.uint8, device="cuda")
+scr = torch.zeros(max(lib.mdp_conv3_scratch_bytes(1, S, cin, cout), 16), dtype=torch.uint8, device="cuda")
 f = lambda: _ext.check(lib.mdp_conv3_layer(0, 1, S, cin, cout, X.data_ptr(), cin // 4, 0, W.data_ptr(), None, 1, Y.data_ptr(), cout // 4, 0, pool, scr.data_ptr(), scr.numel(), _ext.stream()))
 f(); torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
