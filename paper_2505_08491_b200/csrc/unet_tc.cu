@@ -198,7 +198,6 @@ __device__ __forceinline__ void decode_tile(const ConvArgs& A, int tile, int& b,
 __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const ConvArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ bool s_last;  // split-K: this CTA arrived last for its tile
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = sA + (size_t)A.na * A.a_bytes;
@@ -210,6 +209,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
   uint64_t* t_full = b_empty + A.nbs;
   uint64_t* t_empty = t_full + 2;
   uint32_t* tmem_slot = (uint32_t*)(t_empty + 2);
+  volatile uint32_t* s_last = tmem_slot + 1;  // split-K: this CTA arrived last for its tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -396,11 +396,11 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
         if (ew == 0 && lane == 0) {
           const int tkt = (tile / (A.nsplit * A.ksplit)) * A.nsplit + tile % A.nsplit;
           const unsigned old = atomicAdd(&A.tickets[tkt], 1u);
-          s_last = old == (unsigned)(A.ksplit - 1);
-          if (s_last) A.tickets[tkt] = 0u;  // all ksplit arrivals counted: reset for the next launch
+          *s_last = old == (unsigned)(A.ksplit - 1);
+          if (old == (unsigned)(A.ksplit - 1)) A.tickets[tkt] = 0u;  // all arrivals counted: reset
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        finish = s_last;
+        finish = *s_last != 0;
         if (finish) __threadfence();
       }
       // accumulator values of plane zp, channels n0 + 16 cg .. +16: TMEM, or the
