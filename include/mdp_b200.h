@@ -234,9 +234,7 @@ int mdp_conv3_layer(int32_t path, int32_t nb, int32_t S, int32_t cin, int32_t co
                     const float* in, int32_t in_cq, int32_t in_q0, const float* w, const float* bias,
                     int32_t relu, float* out, int32_t out_cq, int32_t out_q0, int32_t pool,
                     void* scratch, size_t scratch_bytes, void* stream);
-/* Scratch bytes mdp_conv3_layer (path 0) needs for split-K partial sums and
- * arrival tickets.  The scratch must be zero-initialised before its first
- * use; every call leaves the ticket area zero again. */
+/* Scratch bytes mdp_conv3_layer (path 0) needs for split-K partial sums. */
 size_t mdp_conv3_scratch_bytes(int32_t nb, int32_t S, int32_t cin, int32_t cout);
 
 /* ------------------------------------------------------------------ */

@@ -321,17 +321,12 @@ UnetPlan unet_plan(int n, int nb, int path) {
     p.o_scr = p.scr_bytes = 0;
   } else {
     p.o_d1 = p.o_e2 = p.o_e3 = 0;
-    // layers share one scratch: room for the largest partial-sum set plus the
-    // largest ticket set (tickets live at the end of the scratch)
-    size_t part = 0, tick = 0;
+    size_t scr = 0;
     const int shp[6][3] = {{n, 16, 32}, {n, 32, 64}, {p.m, 64, 128}, {p.q, 128, 128}, {p.m, 128, 64}, {n, 64, 32}};
     for (auto& L : shp) {
-      const size_t t = tc_conv3_ticket_bytes(nb, L[0], L[1], L[2]);
-      const size_t pb = tc_conv3_scratch_bytes(nb, L[0], L[1], L[2]) - t;
-      part = pb > part ? pb : part;
-      tick = t > tick ? t : tick;
+      size_t b = tc_conv3_scratch_bytes(nb, L[0], L[1], L[2]);
+      scr = b > scr ? b : scr;
     }
-    const size_t scr = part + tick;
     p.scr_bytes = scr;
     p.o_scr = scr ? take(scr) : 0;
   }

@@ -35,11 +35,8 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
 // planes) on tensor cores; w packed [tap][quad][Cout][4] (neural.pack_tconv path 0)
 int tc_tconv(int nb, const float4* in, int in_cq, int cin, int cout, int Sin, int op, const float* w,
              const float* bias, float4* out, int out_cq, int out_q0, cudaStream_t st);
-// scratch needed by the split-K partial sums + tickets of one layer (0 when
-// not split); the tickets sit at the end of the scratch passed to tc_conv3
-// and must be zero before the first use (they are left zero)
+// scratch needed by the split-K partial sums of one layer (0 when not split)
 size_t tc_conv3_scratch_bytes(int nb, int S, int cin, int cout);
-size_t tc_conv3_ticket_bytes(int nb, int S, int cin, int cout);
 
 __device__ __forceinline__ float tf32_round(float f) {
   uint32_t u;

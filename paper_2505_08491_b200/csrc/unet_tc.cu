@@ -45,7 +45,6 @@ struct ConvArgs {
   int nsplit, ncol;  // output channels split over nsplit CTAs of ncol each (small layers)
   int ksplit, cps;   // input-channel chunks split over ksplit CTAs of cps chunks (small layers)
   float4* partial;   // ksplit > 1: raw FP32 partial sums [ks][item][Cout/4][S^3]
-  unsigned int* tickets;  // ksplit > 1: arrivals per (tile, n-slice); zero on entry, left zero
   int tx, ty, tz, ntiles;
   int in_cq, in_q0;
   const float* w;
@@ -209,7 +208,6 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
   uint64_t* t_full = b_empty + A.nbs;
   uint64_t* t_empty = t_full + 2;
   uint32_t* tmem_slot = (uint32_t*)(t_empty + 2);
-  volatile uint32_t* s_last = tmem_slot + 1;  // split-K: this CTA arrived last for its tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -369,10 +367,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
       const int q0 = A.out_q0 + n0 / 4;
       const int gx = x0 + lx, gy = y0 + ly;
       auto zcol = [&](int zp) { return (uint32_t)((A.fold ? ZP - 1 - zp : zp) * A.ncol); };
-      bool finish = true;  // this CTA writes the layer output for the tile
-      if (A.ksplit > 1) {
-        // split-K: raw partial sums; the last of the tile's ksplit CTAs (ticket)
-        // sums them in fixed k order and runs the epilogue below
+      if (A.ksplit > 1) {  // raw partial sums; conv_split_reduce_kernel finishes the layer
 #pragma unroll
         for (int zp = 0; zp < ZP; ++zp) {
           const int gz = z0 + zp;
@@ -389,45 +384,6 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
             }
           }
         }
-        fence_before();
-        mbar_arrive(&t_empty[buf]);  // accumulator free: the next tile's MMAs may start
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps
-        if (ew == 0 && lane == 0) {
-          const int tkt = (tile / (A.nsplit * A.ksplit)) * A.nsplit + tile % A.nsplit;
-          const unsigned old = atomicAdd(&A.tickets[tkt], 1u);
-          *s_last = old == (unsigned)(A.ksplit - 1);
-          if (old == (unsigned)(A.ksplit - 1)) A.tickets[tkt] = 0u;  // all arrivals counted: reset
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        finish = *s_last != 0;
-        if (finish) __threadfence();
-      }
-      // accumulator values of plane zp, channels n0 + 16 cg .. +16: TMEM, or the
-      // fixed-order sum of the split-K partials (invalid voxels read as 0; they
-      // are never stored and never meet a valid voxel in a pool window)
-      auto acc16 = [&](int zp, int cg, float* v) {
-        if (A.ksplit == 1) {
-          tmem_ld16(dcol + zcol(zp) + cg * 16, v);
-          return;
-        }
-        const int gz = z0 + zp;
-        const bool ok = gx < S && gy < S && gz < S;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (ok) {
-            const int64_t off = ((int64_t)b * (A.cout / 4) + n0 / 4 + cg * 4 + q) * S3 + ((int64_t)gz * S + gy) * S + gx;
-            a = __ldcg(A.partial + off);
-            for (int k = 1; k < A.ksplit; ++k) {
-              const float4 p = __ldcg(A.partial + off + (int64_t)k * A.nb * (A.cout / 4) * S3);
-              a.x += p.x; a.y += p.y; a.z += p.z; a.w += p.w;
-            }
-          }
-          v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
-        }
-      };
-      if (!finish) {
       } else if (A.epi == EPI_HEAD) {  // dec1 (ncol == cout == 32) -> head1 -> head2 -> ||r|| * y
         const HeadArgs& H = A.head;
         const int sys = sys_of(H.sel, b);
@@ -437,8 +393,8 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           const int gz = z0 + zp;
           const bool ok = gx < S && gy < S && gz < S;
           float v[32];
-          acc16(zp, 0, v);
-          acc16(zp, 1, v + 16);
+          tmem_ld16(dcol + zcol(zp), v);
+          tmem_ld16(dcol + zcol(zp) + 16, v + 16);
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             float m = v[i];
@@ -457,8 +413,8 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
         const bool writer = ((lane & 1) == 0) && ((ly & 1) == 0) && px < So && py < So && pz < So;
         for (int cg = 0; cg < A.ncol / 16; ++cg) {
           float v0[16], v1[16];
-          acc16(0, cg, v0);
-          acc16(1, cg, v1);
+          tmem_ld16(dcol + cg * 16, v0);
+          tmem_ld16(dcol + A.ncol + cg * 16, v1);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float m = fmaxf(v0[i], v1[i]);
@@ -483,7 +439,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           const bool ok = gx < S && gy < S && gz < S;
           for (int cg = 0; cg < A.ncol / 16; ++cg) {
             float v[16];
-            acc16(zp, cg, v);
+            tmem_ld16(dcol + zcol(zp) + cg * 16, v);
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               float m = v[i];
@@ -501,10 +457,8 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           }
         }
       }
-      if (A.ksplit == 1) {
-        fence_before();
-        mbar_arrive(&t_empty[buf]);
-      }
+      fence_before();
+      mbar_arrive(&t_empty[buf]);
     }
   }
   __syncwarp();
@@ -513,6 +467,73 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
   fence_after();
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(A.tmem_cols));
+  }
+}
+
+// Fixed-order sum of the ksplit partials + bias + ReLU (+ 2x2x2 max pool) +
+// TF32 rounding into the output slot (deterministic: the split count depends
+// on the layer shape, never on the batch).
+__global__ void conv_split_reduce_kernel(const float4* __restrict__ part, int ksplit, int nb, int cq, int S,
+                                         const float* __restrict__ bias, int relu, int pool, float4* __restrict__ out,
+                                         int out_cq, int out_q0) {
+  const int So = pool ? S / 2 : S;
+  const int64_t S3 = (int64_t)S * S * S, So3 = (int64_t)So * So * So;
+  const int64_t total = (int64_t)nb * cq * So3;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t % So3;
+    const int64_t bq = t / So3;
+    const int q = bq % cq, b = bq / cq;
+    const int x = v % So, y = (v / So) % So, z = v / ((int64_t)So * So);
+    const float4 bb = bias ? make_float4(bias[4 * q], bias[4 * q + 1], bias[4 * q + 2], bias[4 * q + 3])
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 m = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    const int nw = pool ? 8 : 1;
+    for (int d = 0; d < nw; ++d) {
+      const int xx = pool ? 2 * x + (d & 1) : x, yy = pool ? 2 * y + ((d >> 1) & 1) : y,
+                zz = pool ? 2 * z + (d >> 2) : z;
+      const int64_t vi = ((int64_t)zz * S + yy) * S + xx;
+      float4 acc = part[((int64_t)b * cq + q) * S3 + vi];
+      for (int k = 1; k < ksplit; ++k) {
+        const float4 p = part[(((int64_t)k * nb + b) * cq + q) * S3 + vi];
+        acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+      }
+      m.x = fmaxf(m.x, acc.x); m.y = fmaxf(m.y, acc.y); m.z = fmaxf(m.z, acc.z); m.w = fmaxf(m.w, acc.w);
+    }
+    m.x += bb.x; m.y += bb.y; m.z += bb.z; m.w += bb.w;
+    if (relu) m = make_float4(fmaxf(m.x, 0.f), fmaxf(m.y, 0.f), fmaxf(m.z, 0.f), fmaxf(m.w, 0.f));
+    out[((int64_t)b * out_cq + out_q0 + q) * So3 + v] = tf32_round4(m);
+  }
+}
+
+// EPI_HEAD after split-K: fixed-order partial sum of the 32 dec1 channels of
+// one voxel + bias + ReLU + TF32 rounding, then the heads and ||r|| scaling.
+__global__ void conv_split_reduce_head_kernel(const float4* __restrict__ part, int ksplit, int nb, int S,
+                                              const float* __restrict__ bias, int relu, const HeadArgs H) {
+  const int64_t S3 = (int64_t)S * S * S;
+  const int64_t total = (int64_t)nb * S3;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t % S3;
+    const int b = t / S3;
+    float d[32];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 acc = part[((int64_t)b * 8 + q) * S3 + v];
+      for (int k = 1; k < ksplit; ++k) {
+        const float4 p = part[(((int64_t)k * nb + b) * 8 + q) * S3 + v];
+        acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+      }
+      const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float m = a[e];
+        if (bias) m += bias[4 * q + e];
+        if (relu) m = fmaxf(m, 0.f);
+        d[4 * q + e] = tf32_round(m);
+      }
+    }
+    const float y = head_eval(d, H.w1, H.b1, H.w2, H.b2);
+    double* zp = H.z + sys_of(H.sel, b) * H.ldz + v;
+    *zp = H.accumulate ? *zp + H.rnorm[b] * (double)y : H.rnorm[b] * (double)y;
   }
 }
 
@@ -667,27 +688,10 @@ static void tc_split(int nb, int S, int cin, int cout, int& nsplit, int& ksplit)
       }
 }
 
-// split-K scratch of one layer: the partial sums, and the tickets (one per
-// tile x n-slice), which tc_conv3 places at the END of the caller's scratch so
-// layers of different shapes sharing one scratch never overlap partials and
-// tickets (the tickets must be zero initially; every launch leaves them zero)
-static size_t tc_partial_bytes(int nb, int S, int cin, int cout, int& ntickets) {
+size_t tc_conv3_scratch_bytes(int nb, int S, int cin, int cout) {
   int ns, ks;
   tc_split(nb, S, cin, cout, ns, ks);
-  ntickets = ks > 1 ? nb * ceil_div(S, tc::BX) * ceil_div(S, tc::BY) * ceil_div(S, tc::ZP) * ns : 0;
-  return ks > 1 ? ((size_t)ks * nb * cout * S * S * S * sizeof(float) + 255) / 256 * 256 : 0;
-}
-
-size_t tc_conv3_scratch_bytes(int nb, int S, int cin, int cout) {
-  int nt;
-  const size_t p = tc_partial_bytes(nb, S, cin, cout, nt);
-  return p + ((size_t)nt * sizeof(unsigned int) + 255) / 256 * 256;
-}
-
-size_t tc_conv3_ticket_bytes(int nb, int S, int cin, int cout) {
-  int nt;
-  tc_partial_bytes(nb, S, cin, cout, nt);
-  return ((size_t)nt * sizeof(unsigned int) + 255) / 256 * 256;
+  return ks > 1 ? (size_t)ks * nb * cout * S * S * S * sizeof(float) : 0;
 }
 
 int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int in_q0, const float* w,
@@ -719,11 +723,9 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   A.cps = A.nchunk / A.ksplit;
   A.ntiles = spatial * A.nsplit * A.ksplit;
   A.partial = (float4*)scratch;
-  if (A.ksplit > 1) {
+  if (A.ksplit > 1)
     MDP_REQUIRE(scratch && scratch_bytes >= tc_conv3_scratch_bytes(nb, S, cin, cout),
                 "split-K conv needs %zu bytes of scratch", tc_conv3_scratch_bytes(nb, S, cin, cout));
-    A.tickets = (unsigned int*)((char*)scratch + scratch_bytes - tc_conv3_ticket_bytes(nb, S, cin, cout));
-  }
   A.in_cq = in_cq;
   A.in_q0 = in_q0;
   A.w = w;
@@ -793,6 +795,22 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   int grid = A.ntiles < sm_count() ? A.ntiles : sm_count();
   conv3_tc_kernel<<<grid, 256, smem, st>>>(map, A);
   MDP_LAUNCH_CHECK("conv3_tc_kernel");
+  if (A.ksplit > 1 && epi == EPI_HEAD) {
+    const int64_t total = (int64_t)nb * S * S * S;
+    int bx = ceil_div(total, 128);
+    bx = bx > 8 * sm_count() ? 8 * sm_count() : bx;
+    conv_split_reduce_head_kernel<<<bx, 128, 0, st>>>(A.partial, A.ksplit, nb, S, bias, relu, A.head);
+    MDP_LAUNCH_CHECK("conv_split_reduce_head_kernel");
+  } else if (A.ksplit > 1) {
+    const int pool = epi == EPI_POOL;
+    const int So = pool ? S / 2 : S;
+    const int64_t total = (int64_t)nb * (cout / 4) * So * So * So;
+    int bx = ceil_div(total, 256);
+    bx = bx > 4 * sm_count() ? 4 * sm_count() : bx;
+    conv_split_reduce_kernel<<<bx, 256, 0, st>>>(A.partial, A.ksplit, nb, cout / 4, S, bias, relu, pool, out,
+                                                 out_cq, out_q0);
+    MDP_LAUNCH_CHECK("conv_split_reduce_kernel");
+  }
   return MDP_OK;
 }
 

@@ -43,7 +43,7 @@ def run_layer(path, x, k, bias, relu=True, pool=False, out_extra_quads=0):
     oq = cout // 4 + out_extra_quads
     Y = torch.full((b, oq, So, So, So, 4), float("nan"), dtype=torch.float32, device="cuda")
     nscr = lib.mdp_conv3_scratch_bytes(b, S, cin, cout)
-    scr = torch.zeros(max(nscr, 16), dtype=torch.uint8, device="cuda")  # tickets must start at zero
+    scr = torch.zeros(max(nscr, 16), dtype=torch.uint8, device="cuda")
     _ext.check(lib.mdp_conv3_layer(path, b, S, cin, cout, X.data_ptr(), cin // 4, 0, W.data_ptr(),
                                    None if Bt is None else Bt.data_ptr(), int(relu), Y.data_ptr(), oq,
                                    out_extra_quads, int(pool), scr.data_ptr(), nscr, _ext.stream()))
