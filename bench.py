@@ -254,6 +254,17 @@ def neural_forward_flops(n):
     return f
 
 
+def ncu_traffic(key):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of a
+    kernel from the committed ncu --set full summary (profiles/traffic.json,
+    written by tools/ncu_summary.py --traffic), or None."""
+    path = Path(__file__).resolve().parent / "profiles" / "traffic.json"
+    try:
+        return json.loads(path.read_text()).get(key)
+    except (OSError, ValueError):
+        return None
+
+
 def spmv_roofline(solver, reps=50):
     """Coupled SpMV: algorithmic bytes 16 (N3 + N1) + 40 Q per system."""
     import torch
@@ -411,7 +422,8 @@ def run_ours(args):
             "applies_per_s": applies_per_s,
             "roofline": {"bound": "tensor", "kernel": f"conv3_tc_kernel ({dom}, S={L['S']})",
                          "achieved": L["tflops"], "peak": tf32, "unit": "TFLOP/s",
-                         "frac": L["tflops"] / tf32, "traffic": None,
+                         "frac": L["tflops"] / tf32,
+                         "traffic": (ncu_traffic(f"conv3_tc_kernel {dom} S={L['S']}") or {}).get("dram_bytes"),
                          "peak_note": "cuBLAS TF32 8192^3 measured in this run",
                          "frac_of_bf16_measured_over_2": L["tflops"] / (pk["bf16_tflops"] / 2)},
             "conv_layers": layers,

@@ -1,6 +1,8 @@
 """Compact summary of ncu --set full reports (.ncu-rep) for profiles/.
 
     python tools/ncu_summary.py out.json a.ncu-rep [b.ncu-rep ...]
+    python tools/ncu_summary.py --traffic profiles/traffic.json "key=rep.ncu-rep" ...
+(the second form records per-launch DRAM bytes under the keys bench.py looks up)
 
 Per report and kernel: duration, DRAM bytes read/written (the `traffic` of
 bench.py's roofline), throughputs, tensor-pipe activity, L2 hit rate,
@@ -57,6 +59,16 @@ def summarise(rep):
 
 
 if __name__ == "__main__":
+    if sys.argv[1] == "--traffic":
+        out = {}
+        for kv in sys.argv[3:]:
+            key, rep = kv.rsplit("=", 1)
+            d = summarise(rep)[0]
+            out[key] = {"dram_bytes": d.get("dram_bytes"), "duration_us": d.get("duration_us"),
+                        "source": rep.rsplit("/", 1)[-1]}
+        json.dump(out, open(sys.argv[2], "w"), indent=1)
+        print(json.dumps(out, indent=1))
+        sys.exit(0)
     allr = {}
     for rep in sys.argv[2:]:
         allr[rep.rsplit("/", 1)[-1]] = summarise(rep)
