@@ -31,14 +31,23 @@ __global__ void pack_input_kernel(const int32_t* sel, const double* __restrict__
   }
 }
 
-// enc1a: 3x3x3 conv 2 -> 16, bias, ReLU (neural.py:343); w [16][2][27]
+// enc1a: 3x3x3 conv 2 -> 16, bias, ReLU (neural.py:343); w [16][2][27].
+// The weights are transposed in shared memory to [tap][ch][16] so one
+// (tap, channel) is four 16-byte broadcast loads feeding 16 FMAs (a scalar
+// load per FMA made this kernel LSU-bound); neighbours are loaded one z-plane
+// (9 taps) at a time, all before their FMAs.
 __global__ void __launch_bounds__(128) enc1a_kernel(const float2* __restrict__ xin, int S,
                                                      const float* __restrict__ w,
                                                      const float* __restrict__ bias,
                                                      float4* __restrict__ out, int round_tf32) {
-  __shared__ float ws[16 * 2 * 27 + 16];
-  for (int t = threadIdx.x; t < 16 * 54; t += blockDim.x) ws[t] = w[t];
-  for (int t = threadIdx.x; t < 16; t += blockDim.x) ws[864 + t] = bias ? bias[t] : 0.f;
+  __shared__ float4 ws4[27 * 2 * 4];  // [tap][ch][16 channels as 4 float4]
+  __shared__ float bs[16];
+  float* wsf = reinterpret_cast<float*>(ws4);
+  for (int t = threadIdx.x; t < 16 * 54; t += blockDim.x) {
+    const int c = t / 54, ch = (t / 27) % 2, tap = t % 27;  // w[(c * 2 + ch) * 27 + tap]
+    wsf[(tap * 2 + ch) * 16 + c] = w[t];
+  }
+  for (int t = threadIdx.x; t < 16; t += blockDim.x) bs[t] = bias ? bias[t] : 0.f;
   __syncthreads();
   const int b = blockIdx.y;
   const int64_t nvox = (int64_t)S * S * S;
@@ -47,22 +56,32 @@ __global__ void __launch_bounds__(128) enc1a_kernel(const float2* __restrict__ x
   const int x = v % S, y = (v / S) % S, z = v / ((int64_t)S * S);
   float acc[16];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) acc[c] = ws[864 + c];
+  for (int c = 0; c < 16; ++c) acc[c] = bs[c];
   const float2* xb = xin + b * nvox;
-  // all 27 neighbour loads are issued before any FMA (latency-bound otherwise);
-  // out-of-domain taps contribute exact zeros (same sums as skipping them)
-  float2 in[27];
 #pragma unroll
-  for (int tap = 0; tap < 27; ++tap) {
-    const int zz = z + tap / 9 - 1, yy = y + (tap / 3) % 3 - 1, xx = x + tap % 3 - 1;
-    const bool ok = zz >= 0 && yy >= 0 && xx >= 0 && zz < S && yy < S && xx < S;
-    in[tap] = ok ? __ldg(xb + ((int64_t)zz * S + yy) * S + xx) : make_float2(0.f, 0.f);
+  for (int dz = 0; dz < 3; ++dz) {
+    // out-of-domain taps contribute exact zeros (same sums as skipping them)
+    float2 in[9];
+    const int zz = z + dz - 1;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const int yy = y + t / 3 - 1, xx = x + t % 3 - 1;
+      const bool ok = zz >= 0 && yy >= 0 && xx >= 0 && zz < S && yy < S && xx < S;
+      in[t] = ok ? __ldg(xb + ((int64_t)zz * S + yy) * S + xx) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const int tap = dz * 9 + t;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 w0 = ws4[(tap * 2 + 0) * 4 + q], w1 = ws4[(tap * 2 + 1) * 4 + q];
+        acc[4 * q + 0] += w0.x * in[t].x + w1.x * in[t].y;
+        acc[4 * q + 1] += w0.y * in[t].x + w1.y * in[t].y;
+        acc[4 * q + 2] += w0.z * in[t].x + w1.z * in[t].y;
+        acc[4 * q + 3] += w0.w * in[t].x + w1.w * in[t].y;
+      }
+    }
   }
-#pragma unroll
-  for (int tap = 0; tap < 27; ++tap)
-#pragma unroll
-    for (int c = 0; c < 16; ++c)
-      acc[c] += ws[(c * 2 + 0) * 27 + tap] * in[tap].x + ws[(c * 2 + 1) * 27 + tap] * in[tap].y;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     float4 o = make_float4(fmaxf(acc[4 * q], 0.f), fmaxf(acc[4 * q + 1], 0.f), fmaxf(acc[4 * q + 2], 0.f),

@@ -26,6 +26,7 @@
 // the epilogue of tile t overlap the MMAs of tile t+1.
 #include <cuda.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "async.cuh"
 #include "unet_layout.cuh"
@@ -68,6 +69,14 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
 
@@ -195,6 +204,7 @@ __device__ __forceinline__ void decode_tile(const ConvArgs& A, int tile, int& b,
 }
 
 __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                          const __grid_constant__ CUtensorMap wmap,
                                                           const ConvArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -225,6 +235,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+    if (A.nsplit > 1) asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -283,11 +294,9 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
             if (A.nsplit == 1) {
               bulk_load(dst, src, A.b_bytes, &b_full[bs]);
             } else {
-              for (int tt = 0; tt < A.tps; ++tt)
-                for (int qd = 0; qd < A.cqc; ++qd)
-                  bulk_load(dst + ((size_t)tt * A.cqc + qd) * A.ncol * 16,
-                            src + (size_t)tt * tap_floats + ((size_t)qd * A.cout + n0) * 4, A.ncol * 16,
-                            &b_full[bs]);
+              // this CTA's ncol output channels of tps taps x cqc quads: one 2-D TMA box
+              // (rows = (chunk, tap, quad), columns = this n-slice) lands as [tap][quad][ncol][4]
+              tma_load_2d(dst, &wmap, &b_full[bs], n0 * 4, (c * nunits + t0) * A.cqc);
             }
             if (++bs == A.nbs) { bs = 0; bp ^= 1; }
           }
@@ -786,6 +795,22 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   MDP_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d) for S=%d cin=%d", (int)r, S, cin);
 
+  // weights as a 2-D tensor (row = (chunk, tap, quad), Cout*4 floats per row) for
+  // the split-N case: one TMA box per weight stage instead of one copy per (tap, quad)
+  CUtensorMap wmap;
+  memset(&wmap, 0, sizeof(wmap));
+  if (A.nsplit > 1) {
+    MDP_REQUIRE(!A.fold, "split-N conv with the z-tap fold layout is not supported");
+    cuuint64_t wdim[2] = {(cuuint64_t)cout * 4, (cuuint64_t)A.nchunk * 27 * A.cqc};
+    cuuint64_t wstride[1] = {(cuuint64_t)cout * 16};
+    cuuint32_t wbox[2] = {(cuuint32_t)A.ncol * 4, (cuuint32_t)(A.tps * A.cqc)};
+    cuuint32_t westr[2] = {1, 1};
+    CUresult rw = enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)w, wdim, wstride, wbox, westr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    MDP_REQUIRE(rw == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d) for the weights", (int)rw);
+  }
+
   const size_t smem = 1024 + (size_t)A.na * A.a_bytes + (size_t)nbs * A.b_bytes + 2048;
   static size_t attr_set = 0;
   if (attr_set < smem) {
@@ -793,7 +818,7 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
     attr_set = 227 * 1024;
   }
   int grid = A.ntiles < sm_count() ? A.ntiles : sm_count();
-  conv3_tc_kernel<<<grid, 256, smem, st>>>(map, A);
+  conv3_tc_kernel<<<grid, 256, smem, st>>>(map, wmap, A);
   MDP_LAUNCH_CHECK("conv3_tc_kernel");
   if (A.ksplit > 1 && epi == EPI_HEAD) {
     const int64_t total = (int64_t)nb * S * S * S;
