@@ -36,10 +36,16 @@ namespace tc {
 
 using namespace ::mdp::async;
 
-constexpr int ZP = 2, BY = 16, BX = 8;
-constexpr int HZ = ZP + 2, HY = BY + 2, HX = BX + 2;
-constexpr int HROWS = HZ * HY * HX;  // 720 halo voxels per quad plane
-constexpr int QUAD_BYTES = HROWS * 16;
+// Brick = ZP x 16 x 8 output voxels; ZP (output z-planes per brick) is a
+// kernel template parameter: 2, or 4 for wide grids of Cout <= 64 layers
+// (half the weight traffic per voxel, halo overhead 1.5x instead of 2x).
+constexpr int BY = 16, BX = 8;
+constexpr int HY = BY + 2, HX = BX + 2;
+template <int ZP>
+struct Brick {
+  static constexpr int HZ = ZP + 2;
+  static constexpr int QUAD_BYTES = HZ * HY * HX * 16;  // one quad plane of the halo brick
+};
 
 struct ConvArgs {
   int nb, S, cin, cout, cqc, nchunk;
@@ -108,10 +114,11 @@ __host__ __device__ constexpr uint32_t tap_off16(int t) {
 // only adds compile-time constants to the 14-bit start-address fields
 // (addresses < 256 KB, no carry), so the single issuing thread spends a few
 // instructions per MMA instead of rebuilding 64-bit descriptors.
-template <int TPS>
+template <int TPS, int ZP>
 __device__ __forceinline__ void issue_stage(uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi,
                                             uint32_t b_tap16, uint32_t b_ks16, uint32_t dcol, uint32_t ncol,
                                             uint32_t idesc, uint32_t& accf) {
+  constexpr uint32_t Q16 = Brick<ZP>::QUAD_BYTES / 16;
 #pragma unroll
   for (int tt = 0; tt < TPS; ++tt) {
 #pragma unroll
@@ -119,7 +126,7 @@ __device__ __forceinline__ void issue_stage(uint32_t a_lo, uint32_t a_hi, uint32
       const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo + tt * b_tap16 + ks * b_ks16);
 #pragma unroll
       for (int zp = 0; zp < ZP; ++zp) {  // one accumulator per z-plane
-        const uint32_t off = tap_off16(tt) + (uint32_t)(zp * HY * HX) + (uint32_t)(ks * 2 * (QUAD_BYTES / 16));
+        const uint32_t off = tap_off16(tt) + (uint32_t)(zp * HY * HX) + (uint32_t)(ks * 2 * Q16);
         const uint64_t ad = ((uint64_t)a_hi << 32) | (a_lo + off);
         mma_tf32(dcol + zp * ncol, ad, bd, idesc, accf);
       }
@@ -131,36 +138,45 @@ __device__ __forceinline__ void issue_stage(uint32_t a_lo, uint32_t a_hi, uint32
 // Start-address offset (16-byte units) of (dy,dx) unit u's view of halo plane 0.
 __host__ __device__ constexpr uint32_t unit_off16(int u) { return (uint32_t)((u / 3) * HX + u % 3); }
 
-// z-tap fold for Cout = 32 layers (A-operand-read bound at N = 32): for one
-// (dy,dx) shift, halo plane hp feeds output plane zp through z-tap dz = hp - zp,
-// so one A read serves both output planes with N = 2*32 (hp = 1, 2) or one
-// plane with N = 32 (hp = 0, 3).  Weights per unit are [quad][dz][Cout][4], so a
-// dz range is a contiguous N range; accumulators are stored descending in zp
-// (plane zp at column (ZP-1-zp)*ncol) so every MMA's D is one contiguous range.
-// hp = 1 goes first: it covers both accumulators, so the tile's first MMA
-// (accumulate = 0) initialises all of D.
-template <int TPS>
+// z-tap fold (Cout <= 64 layers, A-operand-read bound at small N): for one
+// (dy,dx) shift, halo plane hp feeds output planes zp in [hp-2, hp] through
+// z-tap dz = hp - zp, so one A read serves up to three output planes with
+// N = ndz * ncol.  Weights per unit are [quad][dz][ncol][4], so a dz range is
+// a contiguous N range; accumulators are stored descending in zp (plane zp at
+// column (ZP-1-zp)*ncol) so every MMA's D is one contiguous range.  The first
+// MMAs of a tile (accumulate = 0) must initialise every accumulator exactly
+// once: ZP = 2 starts with hp = 1 (planes 0-1); ZP = 4 with hp = 3 (planes
+// 1-3) and hp = 0 (plane 0).
+template <int ZP>
+__device__ __forceinline__ constexpr int fold_hp(int h) {
+  return ZP == 2 ? (h == 0 ? 1 : (h == 1 ? 0 : h)) : (h == 0 ? 3 : (h == 1 ? 0 : (h <= 3 ? h - 1 : h)));
+}
+
+template <int TPS, int ZP>
 __device__ __forceinline__ void issue_stage_fold(uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi,
                                                  uint32_t b_unit16, uint32_t b_ks16, uint32_t dcol, uint32_t ncol,
-                                                 uint32_t idesc1, uint32_t idesc2, uint32_t& accf) {
-  static_assert(ZP == 2, "fold schedule assumes two output planes per brick");
+                                                 const uint32_t* idesc_n, uint32_t& accf) {
+  constexpr uint32_t Q16 = Brick<ZP>::QUAD_BYTES / 16;
+  constexpr int NINIT = ZP == 2 ? 1 : 2;
+  const uint32_t acc0 = accf;
 #pragma unroll
   for (int tt = 0; tt < TPS; ++tt) {
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const int hp = h == 0 ? 1 : (h == 1 ? 0 : h);
-        const int dz_lo = hp == 0 ? 0 : hp - 1;
-        const bool one = hp == 0 || hp == 3;
-        const uint32_t aoff = unit_off16(tt) + (uint32_t)(hp * HY * HX) + (uint32_t)(ks * 2 * (QUAD_BYTES / 16));
+      for (int h = 0; h < ZP + 2; ++h) {
+        const int hp = fold_hp<ZP>(h);
+        const int zlo = hp - 2 > 0 ? hp - 2 : 0, zhi = hp < ZP - 1 ? hp : ZP - 1;
+        const int ndz = zhi - zlo + 1, dz_lo = hp - zhi;
+        const uint32_t aoff = unit_off16(tt) + (uint32_t)(hp * HY * HX) + (uint32_t)(ks * 2 * Q16);
         const uint64_t ad = ((uint64_t)a_hi << 32) | (a_lo + aoff);
         const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo + tt * b_unit16 + ks * b_ks16 + dz_lo * ncol);
-        mma_tf32(dcol + (hp == 0 ? ncol : 0u), ad, bd, one ? idesc1 : idesc2, accf);
-        accf = 1u;
+        const uint32_t a = (tt == 0 && ks == 0 && h < NINIT) ? acc0 : 1u;
+        mma_tf32(dcol + (uint32_t)(ZP - 1 - zhi) * ncol, ad, bd, idesc_n[ndz - 1], a);
       }
     }
   }
+  accf = 1u;
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -186,6 +202,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+template <int ZP>
 __device__ __forceinline__ void decode_tile(const ConvArgs& A, int tile, int& b, int& x0, int& y0, int& z0,
                                             int& n0, int& ks) {
   n0 = (tile % A.nsplit) * A.ncol;
@@ -203,6 +220,7 @@ __device__ __forceinline__ void decode_tile(const ConvArgs& A, int tile, int& b,
   z0 = iz * ZP;
 }
 
+template <int ZP>
 __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const __grid_constant__ CUtensorMap wmap,
                                                           const ConvArgs A) {
@@ -253,7 +271,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
       int as = 0, ap = 0;
       for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
         int b, x0, y0, z0, n0, ks;
-        decode_tile(A, tile, b, x0, y0, z0, n0, ks);
+        decode_tile<ZP>(A, tile, b, x0, y0, z0, n0, ks);
         for (int c = ks * A.cps; c < (ks + 1) * A.cps; ++c) {
           mbar_wait(&a_empty[as], ap ^ 1);
           if (A.dbg & 4) {
@@ -274,7 +292,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
       for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
         if (A.resident && tile != (int)blockIdx.x) break;  // resident filter: loaded once
         int b, x0, y0, z0, n0, ks;
-        decode_tile(A, tile, b, x0, y0, z0, n0, ks);
+        decode_tile<ZP>(A, tile, b, x0, y0, z0, n0, ks);
         for (int c = ks * A.cps; c < (ks + 1) * A.cps; ++c) {
           // packed weights [chunk][tap][quad][cout][4] (fold: [chunk][dydx][quad][dz][cout][4]);
           // a stage holds tps consecutive units: one contiguous copy when the
@@ -296,7 +314,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
             } else {
               // this CTA's ncol output channels of tps taps x cqc quads: one 2-D TMA box
               // (rows = (chunk, tap, quad), columns = this n-slice) lands as [tap][quad][ncol][4]
-              tma_load_2d(dst, &wmap, &b_full[bs], n0 * 4, (c * nunits + t0) * A.cqc);
+              tma_load_2d(dst, &wmap, &b_full[bs], n0 * 4, (c * nunits + t0) * A.cqc * (A.fold ? 3 : 1));
             }
             if (++bs == A.nbs) { bs = 0; bp ^= 1; }
           }
@@ -307,9 +325,10 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
     if (lane == 0) {  // ---------------- MMA issuer
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(A.ncol >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
-      const uint32_t lbo_a = QUAD_BYTES, sbo_a = HX * 16;
+      const uint32_t lbo_a = Brick<ZP>::QUAD_BYTES, sbo_a = HX * 16;
       const uint32_t lbo_b = A.ncol * 16 * (A.fold ? 3 : 1), sbo_b = 128;
-      const uint32_t idesc2 = (idesc & ~(0x3Fu << 17)) | ((uint32_t)((2 * A.ncol) >> 3) << 17);
+      uint32_t idesc_n[3];  // fold: N = 1, 2, 3 x ncol
+      for (int k = 0; k < 3; ++k) idesc_n[k] = (idesc & ~(0x3Fu << 17)) | ((uint32_t)(((k + 1) * A.ncol) >> 3) << 17);
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
       int as = 0, ap = 0, bs = 0, bp = 0, li = 0;
       for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++li) {
@@ -335,16 +354,16 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
             const uint32_t b_ks16 = (uint32_t)(2 * A.ncol * (A.fold ? 3 : 1));         // (2 * lbo_b) / 16
             if (!(A.dbg & 2) && A.fold) {
               switch (A.tps) {
-                case 9: issue_stage_fold<9>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, idesc2, accf); break;
-                case 3: issue_stage_fold<3>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, idesc2, accf); break;
-                default: issue_stage_fold<1>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, idesc2, accf); break;
+                case 9: issue_stage_fold<9, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc_n, accf); break;
+                case 3: issue_stage_fold<3, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc_n, accf); break;
+                default: issue_stage_fold<1, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc_n, accf); break;
               }
             } else if (!(A.dbg & 2)) {
               switch (A.tps) {
-                case 27: issue_stage<27>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
-                case 9: issue_stage<9>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
-                case 3: issue_stage<3>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
-                default: issue_stage<1>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
+                case 27: issue_stage<27, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
+                case 9: issue_stage<9, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
+                case 3: issue_stage<3, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
+                default: issue_stage<1, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
               }
             }
             if (!A.resident) mma_commit(&b_empty[bs]);
@@ -369,7 +388,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
     for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++li) {
       const int buf = li & 1;
       int b, x0, y0, z0, n0, ks;
-      decode_tile(A, tile, b, x0, y0, z0, n0, ks);
+      decode_tile<ZP>(A, tile, b, x0, y0, z0, n0, ks);
       mbar_wait(&t_full[buf], (li >> 1) & 1);
       fence_after();
       const uint32_t dcol = tmem + lane_addr + (uint32_t)(buf * ZP * A.ncol);
@@ -418,26 +437,30 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           }
         }
       } else if (A.epi == EPI_POOL) {
-        const int px = gx >> 1, py = gy >> 1, pz = z0 >> 1;
-        const bool writer = ((lane & 1) == 0) && ((ly & 1) == 0) && px < So && py < So && pz < So;
-        for (int cg = 0; cg < A.ncol / 16; ++cg) {
-          float v0[16], v1[16];
-          tmem_ld16(dcol + cg * 16, v0);
-          tmem_ld16(dcol + A.ncol + cg * 16, v1);
+        const int px = gx >> 1, py = gy >> 1;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float m = fmaxf(v0[i], v1[i]);
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
-            if (A.bias) m += A.bias[n0 + cg * 16 + i];
-            if (A.relu) m = fmaxf(m, 0.f);
-            v0[i] = tf32_round(m);
-          }
-          if (writer && !(A.dbg & 1)) {
+        for (int pp = 0; pp < ZP / 2; ++pp) {  // pooled plane from output planes 2pp, 2pp+1
+          const int pz = (z0 >> 1) + pp;
+          const bool writer = ((lane & 1) == 0) && ((ly & 1) == 0) && px < So && py < So && pz < So;
+          for (int cg = 0; cg < A.ncol / 16; ++cg) {
+            float v0[16], v1[16];
+            tmem_ld16(dcol + zcol(2 * pp) + cg * 16, v0);
+            tmem_ld16(dcol + zcol(2 * pp + 1) + cg * 16, v1);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float4 o = make_float4(v0[4 * q], v0[4 * q + 1], v0[4 * q + 2], v0[4 * q + 3]);
-              A.out[((int64_t)b * A.out_cq + q0 + cg * 4 + q) * So3 + ((int64_t)pz * So + py) * So + px] = o;
+            for (int i = 0; i < 16; ++i) {
+              float m = fmaxf(v0[i], v1[i]);
+              m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+              m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+              if (A.bias) m += A.bias[n0 + cg * 16 + i];
+              if (A.relu) m = fmaxf(m, 0.f);
+              v0[i] = tf32_round(m);
+            }
+            if (writer && !(A.dbg & 1)) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                float4 o = make_float4(v0[4 * q], v0[4 * q + 1], v0[4 * q + 2], v0[4 * q + 3]);
+                A.out[((int64_t)b * A.out_cq + q0 + cg * 4 + q) * So3 + ((int64_t)pz * So + py) * So + px] = o;
+              }
             }
           }
         }
@@ -679,7 +702,7 @@ static EncodeTiledFn encode_fn() {
 // Split decisions for one layer shape (shared by the launch and the workspace plan).
 static void tc_split(int nb, int S, int cin, int cout, int& nsplit, int& ksplit) {
   using namespace tc;
-  const int tiles_item = ceil_div(S, BX) * ceil_div(S, BY) * ceil_div(S, ZP);
+  const int tiles_item = ceil_div(S, BX) * ceil_div(S, BY) * ceil_div(S, 2);  // decided on 2-plane bricks
   const int nchunk = cin / 16;
   nsplit = 1;
   while (nb * tiles_item * nsplit < sm_count() && cout / (2 * nsplit) >= 32) nsplit *= 2;
@@ -723,12 +746,16 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   A.nchunk = cin / (4 * A.cqc);
   A.tx = ceil_div(S, BX);
   A.ty = ceil_div(S, BY);
-  A.tz = ceil_div(S, ZP);
-  const int spatial = nb * A.tx * A.ty * A.tz;
   // small layers (few bricks): split the output channels over CTAs (down to
   // 32 per CTA) and, if still short of the SM count, the input chunks
   tc_split(nb, S, cin, cout, A.nsplit, A.ksplit);
   A.ncol = cout / A.nsplit;
+  // z-tap fold for Cout <= 64 (weights packed [chunk][dydx][quad][dz][Cout][4]);
+  // 4-plane bricks when the layer still has >= 2 bricks per SM with them
+  A.fold = cout <= 64;
+  const int zp = (A.fold && A.ksplit == 1 && nb * A.tx * A.ty * ceil_div(S, 4) * A.nsplit >= 2 * sm_count()) ? 4 : 2;
+  A.tz = ceil_div(S, zp);
+  const int spatial = nb * A.tx * A.ty * A.tz;
   A.cps = A.nchunk / A.ksplit;
   A.ntiles = spatial * A.nsplit * A.ksplit;
   A.partial = (float4*)scratch;
@@ -745,10 +772,9 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   A.out_cq = out_cq;
   A.out_q0 = out_q0;
   A.Sout = epi == EPI_POOL ? S / 2 : S;
-  A.a_bytes = (uint32_t)A.cqc * QUAD_BYTES;
+  A.a_bytes = (uint32_t)A.cqc * (zp == 4 ? Brick<4>::QUAD_BYTES : Brick<2>::QUAD_BYTES);
   A.na = 2;
   const size_t budget = 227 * 1024 - 2048 - 1024;
-  A.fold = cout == 32 && A.nsplit == 1 && epi != EPI_POOL;
   const int nunits = A.fold ? 9 : 27;
   const size_t tap_bytes = (size_t)A.cqc * A.ncol * 16 * (A.fold ? 3 : 1);  // one weight unit
   A.resident = 0;
@@ -771,7 +797,8 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   A.nbs = nbs;
   MDP_REQUIRE((size_t)A.na * A.a_bytes + (size_t)nbs * A.b_bytes <= budget, "tc conv tile does not fit smem");
   uint32_t cols = 32;
-  while (cols < (uint32_t)(2 * ZP * A.ncol)) cols <<= 1;
+  while (cols < (uint32_t)(2 * zp * A.ncol)) cols <<= 1;
+  MDP_REQUIRE(cols <= 512, "conv accumulators need %u TMEM columns", cols);
   A.tmem_cols = cols;
   if (head) A.head = *head;
   {
@@ -788,7 +815,7 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   CUtensorMap map;
   cuuint64_t gdim[4] = {(cuuint64_t)4 * S, (cuuint64_t)S, (cuuint64_t)S, (cuuint64_t)nb * in_cq};
   cuuint64_t gstride[3] = {(cuuint64_t)16 * S, (cuuint64_t)16 * S * S, (cuuint64_t)16 * S * S * S};
-  cuuint32_t box[4] = {4 * HX, HY, HZ, (cuuint32_t)A.cqc};
+  cuuint32_t box[4] = {4 * HX, HY, (cuuint32_t)(zp + 2), (cuuint32_t)A.cqc};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)in, gdim, gstride, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -800,10 +827,10 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   CUtensorMap wmap;
   memset(&wmap, 0, sizeof(wmap));
   if (A.nsplit > 1) {
-    MDP_REQUIRE(!A.fold, "split-N conv with the z-tap fold layout is not supported");
+    // rows: (chunk, tap, quad), or with the fold (chunk, dydx, quad, dz) -- 27 x cqc per chunk either way
     cuuint64_t wdim[2] = {(cuuint64_t)cout * 4, (cuuint64_t)A.nchunk * 27 * A.cqc};
     cuuint64_t wstride[1] = {(cuuint64_t)cout * 16};
-    cuuint32_t wbox[2] = {(cuuint32_t)A.ncol * 4, (cuuint32_t)(A.tps * A.cqc)};
+    cuuint32_t wbox[2] = {(cuuint32_t)A.ncol * 4, (cuuint32_t)(A.tps * A.cqc * (A.fold ? 3 : 1))};
     cuuint32_t westr[2] = {1, 1};
     CUresult rw = enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)w, wdim, wstride, wbox, westr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -812,13 +839,18 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   }
 
   const size_t smem = 1024 + (size_t)A.na * A.a_bytes + (size_t)nbs * A.b_bytes + 2048;
-  static size_t attr_set = 0;
-  if (attr_set < smem) {
-    cudaFuncSetAttribute(conv3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
-    attr_set = 227 * 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(conv3_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+    cudaFuncSetAttribute(conv3_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+    attr_set = true;
   }
+  MDP_REQUIRE(smem <= 227 * 1024, "tc conv needs %zu bytes of shared memory", smem);
   int grid = A.ntiles < sm_count() ? A.ntiles : sm_count();
-  conv3_tc_kernel<<<grid, 256, smem, st>>>(map, wmap, A);
+  if (zp == 4)
+    conv3_tc_kernel<4><<<grid, 256, smem, st>>>(map, wmap, A);
+  else
+    conv3_tc_kernel<2><<<grid, 256, smem, st>>>(map, wmap, A);
   MDP_LAUNCH_CHECK("conv3_tc_kernel");
   if (A.ksplit > 1 && epi == EPI_HEAD) {
     const int64_t total = (int64_t)nb * S * S * S;

@@ -170,7 +170,7 @@ def pack_conv(kernel: np.ndarray, path: int) -> np.ndarray:
         return np.ascontiguousarray(k.reshape(cout // 16, 16, cin, 27).transpose(0, 2, 3, 1))
     cqc = 4  # 16-channel chunks (unet_tc.cu)
     nch = cin // (4 * cqc)
-    if cout == 32:  # z-tap fold (unet_tc.cu issue_stage_fold): [chunk][dydx][quad][dz][cout][4]
+    if cout <= 64:  # z-tap fold (unet_tc.cu issue_stage_fold): [chunk][dydx][quad][dz][cout][4]
         p = k.reshape(cout, nch, cqc, 4, 3, 9).transpose(1, 5, 2, 4, 0, 3)
     else:
         p = k.reshape(cout, nch, cqc, 4, 27).transpose(1, 4, 2, 0, 3)  # [chunk][tap][quad][cout][4]

@@ -82,6 +82,24 @@ def test_conv_pool_epilogue_vs_oracle(gpu, S, cin, cout):
     assert rel(y, ref) <= TF32_TOL
 
 
+@pytest.mark.parametrize("cin,cout,pool", [(16, 32, 0), (64, 32, 0), (32, 64, 1), (128, 64, 0), (64, 128, 1)])
+def test_conv_wide_grid_vs_oracle(gpu, cin, cout, pool):
+    """Grids with >= 2 bricks per SM: 4-plane bricks with the z-tap fold (Cout <= 64),
+    plain 2-plane bricks for Cout = 128."""
+    import oracle
+    S = 40
+    rng = np.random.default_rng(cin * 7 + cout)
+    x = rng.standard_normal((2, cin, S, S, S))
+    k = rng.standard_normal((cout, cin, 3, 3, 3)) * np.sqrt(2.0 / (27 * cin))
+    bias = None if pool else rng.standard_normal(cout) * 0.1
+    ref = np.maximum(oracle.conv3d(x, k, bias), 0.0)
+    if pool:
+        ref = oracle.maxpool3d(ref)
+    y, _ = run_layer(0, x, k, bias, pool=bool(pool))
+    assert y.shape == ref.shape
+    assert rel(y, ref) <= TF32_TOL
+
+
 @pytest.mark.parametrize("path,tol", [(0, TF32_TOL), (1, FP32_TOL)])
 def test_unet_forward_vs_reference(gpu, path, tol):
     from paper_2505_08491_b200 import neural
