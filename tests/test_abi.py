@@ -95,8 +95,11 @@ def test_weight_packing_layouts():
     k = rng.standard_normal((64, 32, 3, 3, 3)).astype(np.float32)
     p1 = neural.pack_conv(k, neural.PATH_CUDA_CORE).reshape(4, 32, 27, 16)
     assert p1[1, 5, 13, 7] == k[16 + 7, 5].ravel()[13]
-    p0 = neural.pack_conv(k, neural.PATH_TCGEN05).reshape(2, 27, 4, 64, 4)
-    assert abs(p0[1, 13, 2, 40, 3] - k[40, 16 + 2 * 4 + 3].ravel()[13]) <= 2e-3 * abs(k[40, 27].ravel()[13])
+    k128 = rng.standard_normal((128, 32, 3, 3, 3)).astype(np.float32)  # Cout = 128: [chunk][tap][quad][cout][4]
+    p0 = neural.pack_conv(k128, neural.PATH_TCGEN05).reshape(2, 27, 4, 128, 4)
+    assert abs(p0[1, 13, 2, 40, 3] - k128[40, 16 + 2 * 4 + 3].ravel()[13]) <= 2e-3 * abs(k128[40, 27].ravel()[13])
+    p64 = neural.pack_conv(k, neural.PATH_TCGEN05).reshape(2, 9, 4, 3, 64, 4)  # Cout <= 64: z-tap fold layout
+    assert abs(p64[1, 4, 2, 1, 40, 3] - k[40, 16 + 2 * 4 + 3, 1, 1, 1]) <= 2e-3 * abs(k[40, 27, 1, 1, 1])
     k32 = rng.standard_normal((32, 64, 3, 3, 3)).astype(np.float32)  # Cout = 32: z-tap fold layout
     pf = neural.pack_conv(k32, neural.PATH_TCGEN05).reshape(4, 9, 4, 3, 32, 4)  # [chunk][dydx][quad][dz][cout][4]
     assert abs(pf[2, 7, 1, 2, 30, 3] - k32[30, 2 * 16 + 1 * 4 + 3, 2, 2, 1]) <= 1e-3 * abs(k32[30, 39, 2, 2, 1])
