@@ -91,6 +91,12 @@ __device__ double g_zero_row[32];  // zero page: out-of-domain rows read from he
 #ifndef STENCIL_PF
 #define STENCIL_PF 2  // planes of loads in flight per warp (tools/stencil_sweep.py A/B)
 #endif
+#ifndef STENCIL_UNROLL
+#define STENCIL_UNROLL 1
+#endif
+#ifndef STENCIL_ROWS
+#define STENCIL_ROWS 2  // output rows per warp
+#endif
 
 struct GatherArgs {  // optional Pi gather folded into the stencil launch (last y-slice)
   const double* x3;
@@ -104,7 +110,7 @@ __global__ void __launch_bounds__(128) stencil_kernel(const mdp_problem P, const
                                                        double* __restrict__ y, int64_t ldy, int zchunk,
                                                        const double* __restrict__ jr, double omega,
                                                        const GatherArgs G) {
-  constexpr int RY = 2, NR = RY + 2, PF = STENCIL_PF;
+  constexpr int RY = STENCIL_ROWS, NR = RY + 2, PF = STENCIL_PF, UNR = STENCIL_UNROLL;
   const int n = P.n;
   const int s = sys_of(sel, blockIdx.z);
   if (GATHER && blockIdx.y == gridDim.y - 1) {  // independent of the stencil: runs alongside it
@@ -173,6 +179,9 @@ __global__ void __launch_bounds__(128) stencil_kernel(const mdp_problem P, const
   double Pm[RY], P0[RY], Rm[RY], R0[RY];
 #pragma unroll
   for (int r = 0; r < RY; ++r) Pm[r] = P0[r] = Rm[r] = R0[r] = 0.0;
+  // unrolled by the ring / recurrence periods so the plane rotation is register
+  // renaming, not moves (the kernel is issue-bound)
+#pragma unroll UNR
   for (int kk = z0 - 1; kk <= z1; ++kk) {
     if (kk + PF <= z1) load(kk + PF, q[PF]);
     double kx[NR], mx[NR];
@@ -484,7 +493,7 @@ static int launch_stencil(const mdp_problem* p, int32_t nsel, const int32_t* sel
                           int64_t ldx, double* y, int64_t ldy, cudaStream_t st, const double* jr = nullptr,
                           double omega = 0.0, const GatherArgs* g = nullptr) {
   const int n = p->n;
-  const int64_t warps = (int64_t)ceil_div(n, 30) * ceil_div(n, 2);  // (x-tile, row pair) per plane
+  const int64_t warps = (int64_t)ceil_div(n, 30) * ceil_div(n, STENCIL_ROWS);  // (x-tile, row group) per plane
   int bx = ceil_div(warps, 4);
   // z-chunks: enough warps to fill the machine; chunks of >= 16 planes when the
   // problem is large, down to 4 planes when it is latency-bound anyway
