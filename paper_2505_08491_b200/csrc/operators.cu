@@ -224,140 +224,6 @@ __global__ void __launch_bounds__(128) stencil_kernel(const mdp_problem P, const
   }
 }
 
-// Variant of stencil_kernel whose plane loads go through a per-warp
-// cp.async (LDGSTS) ring in shared memory, AD planes deep: in-flight data
-// holds no registers and no CTA barrier is involved (each warp owns its ring;
-// cp.async.wait_group + __syncwarp order it).  Same arithmetic per output.
-#ifndef STENCIL_AD
-#define STENCIL_AD 6
-#endif
-template <bool JAC, bool GATHER>
-__global__ void __launch_bounds__(128) stencil_async_kernel(const mdp_problem P, const int32_t* sel,
-                                                             const double* __restrict__ x, int64_t ldx,
-                                                             double* __restrict__ y, int64_t ldy, int zchunk,
-                                                             const double* __restrict__ jr, double omega,
-                                                             const GatherArgs G) {
-  constexpr int RY = 2, NR = RY + 2, AD = STENCIL_AD;
-  __shared__ double ring_all[4][AD][NR][32];
-  const int n = P.n;
-  const int s = sys_of(sel, blockIdx.z);
-  if (GATHER && blockIdx.y == gridDim.y - 1) {
-    gather_rows(P, s, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5), G.x3, G.x1,
-                ldx, G.s_out);
-    return;
-  }
-  const double* xp = x + (int64_t)s * ldx;
-  double* yp = y + (int64_t)s * ldy;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double (*ring)[NR][32] = ring_all[wib];
-  const int tiles_x = (n + 29) / 30;
-  const int wrow = blockIdx.x * (blockDim.x >> 5) + wib;
-  const int j = (wrow / tiles_x) * RY;
-  if (j >= n) return;
-  const int i = (wrow % tiles_x) * 30 - 1 + lane;
-  const int z0 = blockIdx.y * zchunk;
-  const int z1 = min(n, z0 + zchunk);
-  if (z0 >= n) return;
-  const bool dir = P.bc3d != 0;
-  const Line1D c = make_line(P.h);
-  const double kO = P.k_omega, sO = P.sigma_omega;
-  const int64_t nn = (int64_t)n * n;
-  const bool colok = i >= 0 && i < n && !(dir && (i == 0 || i == n - 1));
-  const double* ptr[NR];
-  int64_t step[NR];
-#pragma unroll
-  for (int a = 0; a < NR; ++a) {
-    const int jj = j - 1 + a;
-    const bool ok = colok && jj >= 0 && jj < n && !(dir && (jj == 0 || jj == n - 1));
-    ptr[a] = ok ? xp + (int64_t)(z0 - 1) * nn + (int64_t)jj * n + i : g_zero_row + lane;
-    step[a] = ok ? nn : 0;
-  }
-  auto plane_ok = [&](int kk) { return kk >= 0 && kk < n && !(dir && (kk == 0 || kk == n - 1)); };
-  // issue plane kk into ring slot (kk - z0 + 1) % AD; one commit group per plane (empty groups keep the count)
-  auto issue = [&](int kk) {
-    const int slot = (kk - z0 + 1) % AD;
-    const bool pok = plane_ok(kk);
-#pragma unroll
-    for (int a = 0; a < NR; ++a) {
-      const double* src = pok ? ptr[a] : g_zero_row + lane;
-      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&ring[slot][a][lane]);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-      ptr[a] += step[a];
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  const bool out_lane = lane >= 1 && lane <= 30 && i < n;
-  const int ic = i < 0 ? 0 : (i >= n ? n - 1 : i);
-  const double kdx = kdiag(c, ic, n), mdx = mdiag(c, ic, n);
-  double kdy[RY], mdy[RY];
-  bool rok[RY], colb[RY];
-#pragma unroll
-  for (int r = 0; r < RY; ++r) {
-    const int jr_ = j + r < n ? j + r : n - 1;
-    kdy[r] = kdiag(c, jr_, n);
-    mdy[r] = mdiag(c, jr_, n);
-    rok[r] = out_lane && j + r < n;
-    colb[r] = dir && (i == 0 || i == n - 1 || j + r == 0 || j + r == n - 1);
-  }
-  double* yrow = yp + (int64_t)z0 * nn + (int64_t)j * n + i;
-  const double* xrow = xp + (int64_t)z0 * nn + (int64_t)j * n + i;
-  int64_t goff = (int64_t)s * ldy + (int64_t)z0 * nn + (int64_t)j * n + i;
-#pragma unroll
-  for (int p = 0; p < AD - 1; ++p) {
-    if (z0 - 1 + p <= z1) issue(z0 - 1 + p);
-    else asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  double Pm[RY], P0[RY], Rm[RY], R0[RY];
-#pragma unroll
-  for (int r = 0; r < RY; ++r) Pm[r] = P0[r] = Rm[r] = R0[r] = 0.0;
-  for (int kk = z0 - 1; kk <= z1; ++kk) {
-    // keep AD-1 planes in flight: issue kk+AD-1 (its slot held plane kk-1, consumed last iteration)
-    if (kk + AD - 1 <= z1) issue(kk + AD - 1);
-    else asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group %0;" ::"n"(AD - 1) : "memory");
-    __syncwarp();
-    const int slot = (kk - z0 + 1) % AD;
-    double cur[NR];
-#pragma unroll
-    for (int a = 0; a < NR; ++a) cur[a] = ring[slot][a][lane];
-    __syncwarp();  // everyone has read the slot before it is refilled next iteration
-    double kx[NR], mx[NR];
-#pragma unroll
-    for (int a = 0; a < NR; ++a) {
-      const double lr = __shfl_up_sync(0xffffffffu, cur[a], 1) + __shfl_down_sync(0xffffffffu, cur[a], 1);
-      kx[a] = c.ko * lr + kdx * cur[a];
-      mx[a] = c.mo * lr + mdx * cur[a];
-    }
-    const int ko = kk - 1;
-    const bool emit = ko >= z0;
-    const double kd = kdiag(c, ko < 0 ? 0 : ko, n), md = mdiag(c, ko < 0 ? 0 : ko, n);
-    const bool planeb = dir && (ko == 0 || ko == n - 1);
-#pragma unroll
-    for (int r = 0; r < RY; ++r) {
-      const double msum = mx[r] + mx[r + 2];
-      const double c1 = c.mo * (kx[r] + kx[r + 2]) + mdy[r] * kx[r + 1];
-      const double c2 = c.ko * msum + kdy[r] * mx[r + 1];
-      const double c3 = c.mo * msum + mdy[r] * mx[r + 1];
-      const double Pn = kO * (c1 + c2) + sO * c3;
-      const double Rn = kO * c3;
-      if (emit && rok[r]) {
-        double out = c.mo * (Pm[r] + Pn) + md * P0[r] + c.ko * (Rm[r] + Rn) + kd * R0[r];
-        if (colb[r] || planeb) out = xrow[r * n];
-        if (JAC) out = xrow[r * n] + (omega * (jr[goff + r * n] - out)) / P.diag_c[goff + r * n];
-        yrow[r * n] = out;
-      }
-      Pm[r] = P0[r]; P0[r] = Pn;
-      Rm[r] = R0[r]; R0[r] = Rn;
-    }
-    if (emit) {
-      yrow += nn;
-      xrow += nn;
-      goff += nn;
-    }
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
 __global__ void __launch_bounds__(256) pi_gather_kernel(const mdp_problem P, const int32_t* sel,
                                                          const double* __restrict__ x3,
                                                          const double* __restrict__ x1, int64_t ld,
@@ -516,20 +382,6 @@ static int launch_stencil(const mdp_problem* p, int32_t nsel, const int32_t* sel
   if (gat) bx = bx > ceil_div(p->qmax, 4) ? bx : ceil_div(p->qmax, 4);  // one warp per Pi row in the gather slice
   dim3 grid(bx, zch + (gat ? 1 : 0), nsel);
   GatherArgs G = gat ? *g : GatherArgs{nullptr, nullptr, nullptr};
-#ifndef STENCIL_ASYNC
-#define STENCIL_ASYNC 0
-#endif
-  if (STENCIL_ASYNC && n >= 48) {
-    if (jr) {
-      if (gat) stencil_async_kernel<true, true><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
-      else stencil_async_kernel<true, false><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
-    } else {
-      if (gat) stencil_async_kernel<false, true><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
-      else stencil_async_kernel<false, false><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
-    }
-    MDP_LAUNCH_CHECK("stencil_async_kernel");
-    return MDP_OK;
-  }
   if (jr) {
     if (gat)
       stencil_kernel<true, true><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
