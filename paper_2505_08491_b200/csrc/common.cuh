@@ -40,6 +40,35 @@ inline int check_launch(const char* what) {
 
 __device__ __forceinline__ int sys_of(const int32_t* sel, int i) { return sel ? sel[i] : i; }
 
+// Programmatic dependent launch: every kernel is launched with programmatic
+// stream serialisation (also inside captured CUDA graphs), so the next grid
+// is scheduled while this one drains.  Each kernel enters with
+// MDP_PDL_ENTER(): wait until the preceding grid has completed and its memory
+// is visible, then allow the following grid to launch.  Nothing touches
+// global memory before the wait, so the ordering is the plain stream order.
+#define MDP_PDL_ENTER()                                             \
+  do {                                                              \
+    asm volatile("griddepcontrol.wait;" ::: "memory");              \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+  } while (0)
+
+bool pdl_enabled();  // MDP_PDL=0 disables the attribute (A/B timing)
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
+
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 int sm_count();

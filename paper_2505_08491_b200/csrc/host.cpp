@@ -4,6 +4,7 @@
 // Compiled with -ffp-contract=off so the factorisation performs exactly the
 // reference's rounded operations (krylov.py:188-216) and the factor -- hence
 // the device sweeps -- matches the reference bitwise.
+#include <stdlib.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdarg.h>
@@ -28,6 +29,15 @@ void set_error(const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MDP_PDL");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on != 0;
 }
 
 int sm_count() {

@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
                                                          const double* __restrict__ coef, int cstride,
                                                          double* __restrict__ partial, int pstride,
                                                          unsigned int* ticket, RedOut R) {
+  MDP_PDL_ENTER();
   constexpr int NACC = (MODE == DOT || MODE == UPD_DOT) ? (NV > 0 ? NV : 1) : 1;
   __shared__ double csh[NV > 0 ? NV : 1];
   __shared__ double wsum[4][NACC];
@@ -258,6 +259,7 @@ __global__ void arnoldi_next_kernel(const int32_t* sel, double* V, int64_t ldv_s
                                     const int32_t* __restrict__ nvs, int kmax,
                                     const double* __restrict__ w, int64_t ldw, int64_t n,
                                     const double* __restrict__ hcol, double* vcur, int64_t ldc) {
+  MDP_PDL_ENTER();
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
   const int nv = nvs[i];
@@ -279,7 +281,7 @@ static void launch_orth(int nv_max, dim3 grid, cudaStream_t st, const int32_t* s
                         int64_t n, const double* coef, int cstride, double* partial, int pstride,
                         unsigned int* ticket, const RedOut& R) {
 #define MDP_ORTH(NVT)                                                                            \
-  orth_pass_kernel<NVT, MODE><<<grid, 128, 0, st>>>(sel, V, ldv_sys, ldv_vec, nvs, w, ldw, n, \
+  ::mdp::launch_k(orth_pass_kernel<NVT, MODE>, grid, 128, 0, st, sel, V, ldv_sys, ldv_vec, nvs, w, ldw, n, \
                                                     coef, cstride, partial, pstride, ticket, R)
   if (MODE == NORM) {
     MDP_ORTH(0);
@@ -302,6 +304,7 @@ static void launch_orth(int nv_max, dim3 grid, cudaStream_t st, const int32_t* s
 __global__ void scale_kernel(const int32_t* sel, const double* __restrict__ x, int64_t ldx,
                              const double* __restrict__ num, const double* __restrict__ den,
                              double* __restrict__ y, int64_t ldy, int64_t n) {
+  MDP_PDL_ENTER();
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
   const double* xs = x + s * ldx;
@@ -316,6 +319,7 @@ __global__ void basis_update_kernel(const int32_t* sel, double* x, int64_t ldx,
                                     const double* __restrict__ Z, int64_t ldz_sys, int64_t ldz_vec,
                                     const int32_t* __restrict__ cnt, const double* __restrict__ y,
                                     int ystride, int64_t n) {
+  MDP_PDL_ENTER();
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
   const int c = cnt[i];
@@ -336,6 +340,7 @@ __global__ void __launch_bounds__(128) residual_kernel(const int32_t* sel, const
                                                         const double* __restrict__ y, double* r,
                                                         int64_t ld, int64_t n, double* partial,
                                                         unsigned int* ticket, RedOut R) {
+  MDP_PDL_ENTER();
   __shared__ double sh[32];
   __shared__ double mine[1];
   const int i = blockIdx.y;
@@ -355,6 +360,7 @@ __global__ void __launch_bounds__(128) residual_kernel(const int32_t* sel, const
 
 __global__ void axpby_kernel(const int32_t* sel, double a, const double* __restrict__ x, double b,
                              double* y, int64_t ld, int64_t n) {
+  MDP_PDL_ENTER();
   const int s = sys_of(sel, blockIdx.y);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -366,6 +372,7 @@ __global__ void axpby_kernel(const int32_t* sel, double a, const double* __restr
 __global__ void copy_vec_kernel(const int32_t* sel, const double* __restrict__ src, int64_t lds,
                                 double* __restrict__ dst, int64_t ldd, const int32_t* __restrict__ slot,
                                 int64_t slot_stride, int64_t n) {
+  MDP_PDL_ENTER();
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
   const double* a = src + s * lds;
@@ -383,6 +390,7 @@ __global__ void copy_vec_kernel(const int32_t* sel, const double* __restrict__ s
 __global__ void __launch_bounds__(256) ilu0_apply_kernel(const mdp_ilu F, const int32_t* sel,
                                                           const double* __restrict__ r,
                                                           double* __restrict__ z, int64_t ld, int staged) {
+  MDP_PDL_ENTER();
   extern __shared__ double xsh[];
   const int s = sys_of(sel, blockIdx.x);
   const int rs = F.row_start[s], nrow = F.row_start[s + 1] - rs;
@@ -442,6 +450,7 @@ __global__ void __launch_bounds__(256) ilu0_apply_kernel(const mdp_ilu F, const 
 // (any nonzero flag sends the system through the host-driven exact path).
 __global__ void fixed_init_kernel(int nsel, int k, const double* __restrict__ beta, double* H, double* cs,
                                   double* sn, double* g, double* flag) {
+  MDP_PDL_ENTER();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nsel) return;
   for (int t = 0; t < (k + 1) * k; ++t) H[(int64_t)i * (k + 1) * k + t] = 0.0;
@@ -453,6 +462,7 @@ __global__ void fixed_init_kernel(int nsel, int k, const double* __restrict__ be
 
 __global__ void givens_step_kernel(int nsel, int k, int j, const double* __restrict__ hcol, double* H, double* cs,
                                    double* sn, double* g, double* flag) {
+  MDP_PDL_ENTER();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nsel || flag[i] != 0.0) return;
   double* Hi = H + (int64_t)i * (k + 1) * k;
@@ -484,6 +494,7 @@ __global__ void givens_step_kernel(int nsel, int k, int j, const double* __restr
 // y = H[:m,:m]^-1 g[:m] by back substitution (krylov.py:168-171)
 __global__ void backsub_kernel(int nsel, int k, int m, const double* __restrict__ H, const double* __restrict__ g,
                                const double* __restrict__ flag, double* y) {
+  MDP_PDL_ENTER();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nsel) return;
   const double* Hi = H + (int64_t)i * (k + 1) * k;
@@ -502,6 +513,7 @@ __global__ void backsub_kernel(int nsel, int k, int m, const double* __restrict_
 __global__ void copy_slot_kernel(const int32_t* sel, const double* __restrict__ src, int64_t lds,
                                  const int32_t* __restrict__ slot, int64_t slot_stride, double* __restrict__ dst,
                                  int64_t ldd, int64_t n) {
+  MDP_PDL_ENTER();
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
   const double* a = src + s * lds + (int64_t)slot[i] * slot_stride;
@@ -511,6 +523,7 @@ __global__ void copy_slot_kernel(const int32_t* sel, const double* __restrict__ 
 }
 
 __global__ void fill_kernel(const int32_t* sel, double* y, int64_t ld, int64_t n, double v) {
+  MDP_PDL_ENTER();
   const int s = sys_of(sel, blockIdx.y);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     y[s * ld + e] = v;
@@ -592,7 +605,7 @@ extern "C" int mdp_arnoldi(int32_t nsel, const int32_t* sel, double* V, int64_t 
   launch_orth<UPD_NORM>(nvmax, grid, st, sel, V, ldv_sys, ldv_vec, nv, w, ldw, n, W.h2, kmax + 1, W.partial,
                         pstride, W.ticket, R);
   MDP_LAUNCH_CHECK("orth_pass UPD_NORM");
-  arnoldi_next_kernel<<<ew_grid(n, nsel), 256, 0, st>>>(sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n,
+  ::mdp::launch_k(arnoldi_next_kernel, ew_grid(n, nsel), 256, 0, st, sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n,
                                                          hcol, vcur, ldc);
   MDP_LAUNCH_CHECK("mdp_arnoldi");
   return MDP_OK;
@@ -610,7 +623,7 @@ extern "C" int mdp_norms(int32_t nsel, const int32_t* sel, const double* x, int6
   R.out = out;
   R.ostride = 1;
   R.mode = 1;
-  orth_pass_kernel<0, NORM><<<dim3(nb, nsel), 128, 0, st>>>(sel, nullptr, 0, 0, nullptr, const_cast<double*>(x),
+  ::mdp::launch_k(orth_pass_kernel<0, NORM>, dim3(nb, nsel), 128, 0, st, sel, nullptr, 0, 0, nullptr, const_cast<double*>(x),
                                                             ldx, n, nullptr, 0, W.partial, 1, W.ticket, R);
   MDP_LAUNCH_CHECK("mdp_norms");
   return MDP_OK;
@@ -621,7 +634,7 @@ extern "C" int mdp_scale(int32_t nsel, const int32_t* sel, const double* x, int6
                          void* stream) {
   if (nsel == 0) return MDP_OK;
   MDP_REQUIRE(num || den, "scale needs num or den");
-  scale_kernel<<<ew_grid(n, nsel), 256, 0, (cudaStream_t)stream>>>(sel, x, ldx, num, den, y, ldy, n);
+  ::mdp::launch_k(scale_kernel, ew_grid(n, nsel), 256, 0, (cudaStream_t)stream, sel, x, ldx, num, den, y, ldy, n);
   MDP_LAUNCH_CHECK("mdp_scale");
   return MDP_OK;
 }
@@ -630,7 +643,7 @@ extern "C" int mdp_basis_update(int32_t nsel, const int32_t* sel, double* x, int
                                 const double* Z, int64_t ldz_sys, int64_t ldz_vec, const int32_t* cnt,
                                 const double* y, int32_t ystride, int64_t n, void* stream) {
   if (nsel == 0) return MDP_OK;
-  basis_update_kernel<<<ew_grid(n, nsel), 256, 0, (cudaStream_t)stream>>>(sel, x, ldx, Z, ldz_sys,
+  ::mdp::launch_k(basis_update_kernel, ew_grid(n, nsel), 256, 0, (cudaStream_t)stream, sel, x, ldx, Z, ldz_sys,
                                                                           ldz_vec, cnt, y, ystride, n);
   MDP_LAUNCH_CHECK("mdp_basis_update");
   return MDP_OK;
@@ -647,7 +660,7 @@ extern "C" int mdp_residual(int32_t nsel, const int32_t* sel, const double* b, c
   R.ostride = 1;
   R.nk = 1;
   R.mode = 1;
-  residual_kernel<<<dim3(nb, nsel), 128, 0, st>>>(sel, b, y, r, ld, n, W.partial, W.ticket, R);
+  ::mdp::launch_k(residual_kernel, dim3(nb, nsel), 128, 0, st, sel, b, y, r, ld, n, W.partial, W.ticket, R);
   MDP_LAUNCH_CHECK("mdp_residual");
   return MDP_OK;
 }
@@ -655,7 +668,7 @@ extern "C" int mdp_residual(int32_t nsel, const int32_t* sel, const double* b, c
 extern "C" int mdp_axpby(int32_t nsel, const int32_t* sel, double a, const double* x, double b,
                          double* y, int64_t ld, int64_t n, void* stream) {
   if (nsel == 0) return MDP_OK;
-  axpby_kernel<<<ew_grid(n, nsel), 256, 0, (cudaStream_t)stream>>>(sel, a, x, b, y, ld, n);
+  ::mdp::launch_k(axpby_kernel, ew_grid(n, nsel), 256, 0, (cudaStream_t)stream, sel, a, x, b, y, ld, n);
   MDP_LAUNCH_CHECK("mdp_axpby");
   return MDP_OK;
 }
@@ -664,7 +677,7 @@ extern "C" int mdp_copy_vec(int32_t nsel, const int32_t* sel, const double* src,
                             double* dst, int64_t ldd, const int32_t* dst_slot, int64_t slot_stride,
                             int64_t n, void* stream) {
   if (nsel == 0) return MDP_OK;
-  copy_vec_kernel<<<ew_grid(n, nsel), 256, 0, (cudaStream_t)stream>>>(sel, src, lds, dst, ldd, dst_slot,
+  ::mdp::launch_k(copy_vec_kernel, ew_grid(n, nsel), 256, 0, (cudaStream_t)stream, sel, src, lds, dst, ldd, dst_slot,
                                                                       slot_stride, n);
   MDP_LAUNCH_CHECK("mdp_copy_vec");
   return MDP_OK;
@@ -673,7 +686,7 @@ extern "C" int mdp_copy_vec(int32_t nsel, const int32_t* sel, const double* src,
 extern "C" int mdp_fixed_init(int32_t nsel, int32_t k, const double* beta, double* H, double* cs, double* sn,
                               double* g, double* flag, void* stream) {
   if (nsel == 0) return MDP_OK;
-  fixed_init_kernel<<<ceil_div(nsel, 64), 64, 0, (cudaStream_t)stream>>>(nsel, k, beta, H, cs, sn, g, flag);
+  ::mdp::launch_k(fixed_init_kernel, ceil_div(nsel, 64), 64, 0, (cudaStream_t)stream, nsel, k, beta, H, cs, sn, g, flag);
   MDP_LAUNCH_CHECK("fixed_init_kernel");
   return MDP_OK;
 }
@@ -682,7 +695,7 @@ extern "C" int mdp_givens_step(int32_t nsel, int32_t k, int32_t j, const double*
                                double* sn, double* g, double* flag, void* stream) {
   MDP_REQUIRE(j >= 0 && j < k, "givens column %d outside [0, %d)", j, k);
   if (nsel == 0) return MDP_OK;
-  givens_step_kernel<<<ceil_div(nsel, 64), 64, 0, (cudaStream_t)stream>>>(nsel, k, j, hcol, H, cs, sn, g, flag);
+  ::mdp::launch_k(givens_step_kernel, ceil_div(nsel, 64), 64, 0, (cudaStream_t)stream, nsel, k, j, hcol, H, cs, sn, g, flag);
   MDP_LAUNCH_CHECK("givens_step_kernel");
   return MDP_OK;
 }
@@ -691,7 +704,7 @@ extern "C" int mdp_backsub(int32_t nsel, int32_t k, int32_t m, const double* H, 
                            const double* flag, double* y, void* stream) {
   MDP_REQUIRE(m >= 0 && m <= k, "back substitution size %d outside [0, %d]", m, k);
   if (nsel == 0) return MDP_OK;
-  backsub_kernel<<<ceil_div(nsel, 64), 64, 0, (cudaStream_t)stream>>>(nsel, k, m, H, g, flag, y);
+  ::mdp::launch_k(backsub_kernel, ceil_div(nsel, 64), 64, 0, (cudaStream_t)stream, nsel, k, m, H, g, flag, y);
   MDP_LAUNCH_CHECK("backsub_kernel");
   return MDP_OK;
 }
@@ -700,7 +713,7 @@ extern "C" int mdp_copy_slot(int32_t nsel, const int32_t* sel, const double* src
                              const int32_t* slot, int64_t slot_stride, double* dst, int64_t ldd, int64_t n,
                              void* stream) {
   if (nsel == 0) return MDP_OK;
-  copy_slot_kernel<<<ew_grid(n, nsel), 256, 0, (cudaStream_t)stream>>>(sel, src, lds, slot, slot_stride, dst, ldd,
+  ::mdp::launch_k(copy_slot_kernel, ew_grid(n, nsel), 256, 0, (cudaStream_t)stream, sel, src, lds, slot, slot_stride, dst, ldd,
                                                                        n);
   MDP_LAUNCH_CHECK("copy_slot_kernel");
   return MDP_OK;
@@ -709,7 +722,7 @@ extern "C" int mdp_copy_slot(int32_t nsel, const int32_t* sel, const double* src
 extern "C" int mdp_fill(int32_t nsel, const int32_t* sel, double* y, int64_t ld, int64_t n, double v,
                         void* stream) {
   if (nsel == 0) return MDP_OK;
-  fill_kernel<<<ew_grid(n, nsel), 256, 0, (cudaStream_t)stream>>>(sel, y, ld, n, v);
+  ::mdp::launch_k(fill_kernel, ew_grid(n, nsel), 256, 0, (cudaStream_t)stream, sel, y, ld, n, v);
   MDP_LAUNCH_CHECK("fill_kernel");
   return MDP_OK;
 }
@@ -729,7 +742,7 @@ extern "C" int mdp_ilu0_apply(const mdp_ilu* f, int32_t nsel, const int32_t* sel
     cudaFuncSetAttribute(ilu0_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
     attr = true;
   }
-  ilu0_apply_kernel<<<nsel, 256, staged ? full : base, (cudaStream_t)stream>>>(*f, sel, r, z, ld, staged);
+  ::mdp::launch_k(ilu0_apply_kernel, nsel, 256, staged ? full : base, (cudaStream_t)stream, *f, sel, r, z, ld, staged);
   MDP_LAUNCH_CHECK("mdp_ilu0_apply");
   return MDP_OK;
 }

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(128) stencil_kernel(const mdp_problem P, const
                                                        double* __restrict__ y, int64_t ldy, int zchunk,
                                                        const double* __restrict__ jr, double omega,
                                                        const GatherArgs G) {
+  MDP_PDL_ENTER();
   constexpr int RY = STENCIL_ROWS, NR = RY + 2, PF = STENCIL_PF, UNR = STENCIL_UNROLL;
   const int n = P.n;
   const int s = sys_of(sel, blockIdx.z);
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__(256) pi_gather_kernel(const mdp_problem P, con
                                                          const double* __restrict__ x3,
                                                          const double* __restrict__ x1, int64_t ld,
                                                          double* __restrict__ s_out) {
+  MDP_PDL_ENTER();
   const int s = sys_of(sel, blockIdx.y);
   gather_rows(P, s, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5), x3, x1, ld,
               s_out);
@@ -295,6 +297,7 @@ __global__ void __launch_bounds__(256) coupling_phase2_kernel(const mdp_problem 
                                                                const double* __restrict__ div,
                                                                const double* __restrict__ x1,
                                                                double* __restrict__ y1) {
+  MDP_PDL_ENTER();
   const int s = sys_of(sel, blockIdx.y);
   if ((int)blockIdx.x < bpull) {
     pull_rows(P, s, blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3), bpull * (blockDim.x >> 3), sv, alpha, y3,
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(256) coupling_phase2_kernel(const mdp_problem 
 __global__ void jacobi_update_kernel(const mdp_problem P, const int32_t* sel, const double* __restrict__ r,
                                      const double* __restrict__ x, const double* __restrict__ cx,
                                      double* __restrict__ xo, double omega) {
+  MDP_PDL_ENTER();
   const int s = sys_of(sel, blockIdx.y);
   const int64_t n3 = (int64_t)P.n * P.n * P.n;
   const int64_t base = (int64_t)s * P.ld;
@@ -326,6 +330,7 @@ __global__ void jacobi_update_kernel(const mdp_problem P, const int32_t* sel, co
 // min over segments of |p - (a + clip((p-a).ab / ab.ab, 0, 1) ab)|
 __global__ void __launch_bounds__(256) distance_kernel(int n, const double* __restrict__ seg, int nseg,
                                                         double* __restrict__ out) {
+  MDP_PDL_ENTER();
   __shared__ double sh[256 * 6];
   const int64_t n3 = (int64_t)n * n * n;
   const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -384,14 +389,14 @@ static int launch_stencil(const mdp_problem* p, int32_t nsel, const int32_t* sel
   GatherArgs G = gat ? *g : GatherArgs{nullptr, nullptr, nullptr};
   if (jr) {
     if (gat)
-      stencil_kernel<true, true><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
+      ::mdp::launch_k(stencil_kernel<true, true>, grid, 128, 0, st, *p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
     else
-      stencil_kernel<true, false><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
+      ::mdp::launch_k(stencil_kernel<true, false>, grid, 128, 0, st, *p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
   } else {
     if (gat)
-      stencil_kernel<false, true><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
+      ::mdp::launch_k(stencil_kernel<false, true>, grid, 128, 0, st, *p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
     else
-      stencil_kernel<false, false><<<grid, 128, 0, st>>>(*p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
+      ::mdp::launch_k(stencil_kernel<false, false>, grid, 128, 0, st, *p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);
   }
   MDP_LAUNCH_CHECK("stencil_kernel");
   return MDP_OK;
@@ -401,7 +406,7 @@ static int launch_gather(const mdp_problem* p, int32_t nsel, const int32_t* sel,
                          const double* x1, int64_t ld, double* s, cudaStream_t st) {
   if (p->qmax <= 0) return MDP_OK;
   dim3 grid(ceil_div(p->qmax, 8), nsel);
-  pi_gather_kernel<<<grid, 256, 0, st>>>(*p, sel, x3, x1, ld, s);
+  ::mdp::launch_k(pi_gather_kernel, grid, 256, 0, st, *p, sel, x3, x1, ld, s);
   MDP_LAUNCH_CHECK("pi_gather_kernel");
   return MDP_OK;
 }
@@ -414,7 +419,7 @@ static int launch_phase2(const mdp_problem* p, int32_t nsel, const int32_t* sel,
   const int boned = (y1 && p->r1max > 0) ? ceil_div(p->r1max, 64) : 0;
   if (bpull + boned == 0) return MDP_OK;
   dim3 grid(bpull + boned, nsel);
-  coupling_phase2_kernel<<<grid, 256, 0, st>>>(*p, sel, bpull, s, alpha, y3, ld, div, x1, y1);
+  ::mdp::launch_k(coupling_phase2_kernel, grid, 256, 0, st, *p, sel, bpull, s, alpha, y3, ld, div, x1, y1);
   MDP_LAUNCH_CHECK("coupling_phase2_kernel");
   return MDP_OK;
 }
@@ -434,7 +439,7 @@ using namespace mdp;
 extern "C" int mdp_distance_field(int32_t n, const double* seg, int32_t nseg, double* out, void* stream) {
   MDP_REQUIRE(n >= 2 && nseg >= 1, "distance field needs n>=2 and at least one segment");
   const int64_t n3 = (int64_t)n * n * n;
-  distance_kernel<<<ceil_div(n3, 256), 256, 0, (cudaStream_t)stream>>>(n, seg, nseg, out);
+  ::mdp::launch_k(distance_kernel, ceil_div(n3, 256), 256, 0, (cudaStream_t)stream, n, seg, nseg, out);
   MDP_LAUNCH_CHECK("distance_kernel");
   return MDP_OK;
 }
@@ -507,7 +512,7 @@ extern "C" int mdp_jacobi_sweep(const mdp_problem* p, int32_t nsel, const int32_
   const int64_t n3 = (int64_t)p->n * p->n * p->n;
   int bx = ceil_div(n3, 256);
   bx = bx > 4096 ? 4096 : bx;
-  jacobi_update_kernel<<<dim3(bx, nsel), 256, 0, st>>>(*p, sel, r, x, tmp, x_out, omega);
+  ::mdp::launch_k(jacobi_update_kernel, dim3(bx, nsel), 256, 0, st, *p, sel, r, x, tmp, x_out, omega);
   MDP_LAUNCH_CHECK("jacobi_update_kernel");
   return MDP_OK;
 }

@@ -20,6 +20,7 @@ namespace mdp {
 __global__ void pack_input_kernel(const int32_t* sel, const double* __restrict__ r, int64_t ld,
                                   const double* __restrict__ rnorm, const double* __restrict__ dist,
                                   int64_t ldd, float2* __restrict__ xin, int64_t nvox) {
+  MDP_PDL_ENTER();
   const int b = blockIdx.y;
   const int s = sys_of(sel, b);
   double nr = rnorm[b];
@@ -40,6 +41,7 @@ __global__ void __launch_bounds__(128) enc1a_kernel(const float2* __restrict__ x
                                                      const float* __restrict__ w,
                                                      const float* __restrict__ bias,
                                                      float4* __restrict__ out, int round_tf32) {
+  MDP_PDL_ENTER();
   __shared__ float4 ws4[27 * 2 * 4];  // [tap][ch][16 channels as 4 float4]
   __shared__ float bs[16];
   float* wsf = reinterpret_cast<float*>(ws4);
@@ -118,6 +120,7 @@ __global__ void __launch_bounds__(128) conv3_direct_kernel(const float4* __restr
                                                             const float* __restrict__ bias, int relu,
                                                             float4* __restrict__ out, int out_cq,
                                                             int out_q0) {
+  MDP_PDL_ENTER();
   extern __shared__ float wsh[];  // [32 cin][27][16] chunk
   const int g = blockIdx.y;       // cout group of 16
   const int b = blockIdx.z;
@@ -168,6 +171,7 @@ __global__ void __launch_bounds__(128) conv3_direct_kernel(const float4* __restr
 // 2x2x2 max pool with floor (neural.py:275-290)
 __global__ void maxpool_kernel(const float4* __restrict__ in, int in_cq, int S, int cq,
                                float4* __restrict__ out, int out_cq, int out_q0, int nb) {
+  MDP_PDL_ENTER();
   const int M = S / 2;
   const int64_t mv = (int64_t)M * M * M;
   const int64_t total = (int64_t)nb * cq * mv;
@@ -196,6 +200,7 @@ __global__ void __launch_bounds__(128) tconv_kernel(const float4* __restrict__ i
                                                      const float* __restrict__ bias,
                                                      float4* __restrict__ out, int out_cq, int out_q0,
                                                      int round_tf32, int nmain) {
+  MDP_PDL_ENTER();
   __shared__ float4 wsh[128 * 4];  // [cin][16] for this tap
   const int tap = blockIdx.y & 7, g = blockIdx.y >> 3, b = blockIdx.z;
   if ((int)blockIdx.x >= nmain) {  // tail blocks: the output-padding planes
@@ -258,6 +263,7 @@ __global__ void __launch_bounds__(128) head_kernel(const float4* __restrict__ d1
                                                     const float* __restrict__ w2, const float* __restrict__ b2,
                                                     const int32_t* sel, const double* __restrict__ rnorm,
                                                     double* __restrict__ z, int64_t ldz, int accumulate) {
+  MDP_PDL_ENTER();
   __shared__ float ws[16 * 32 + 16 + 16 + 1];
   for (int t = threadIdx.x; t < 512; t += blockDim.x) ws[t] = w1[t];
   for (int t = threadIdx.x; t < 16; t += blockDim.x) {
@@ -295,7 +301,7 @@ static int direct_conv(int nb, int S, int cin, int cout, const float4* in, int i
     attr = true;
   }
   dim3 grid(ceil_div(nvox, 128), cout / 16, nb);
-  conv3_direct_kernel<<<grid, 128, smem, st>>>(in, in_cq, in_q0, cin, S, w, bias, relu, out, out_cq, out_q0);
+  ::mdp::launch_k(conv3_direct_kernel, grid, 128, smem, st, in, in_cq, in_q0, cin, S, w, bias, relu, out, out_cq, out_q0);
   MDP_LAUNCH_CHECK("conv3_direct_kernel");
   return MDP_OK;
 }
@@ -306,7 +312,7 @@ static int launch_pool(const float4* in, int in_cq, int S, int cq, float4* out, 
   int64_t total = (int64_t)nb * cq * M * M * M;
   int bx = ceil_div(total, 256);
   bx = bx > 8 * sm_count() ? 8 * sm_count() : bx;
-  maxpool_kernel<<<bx, 256, 0, st>>>(in, in_cq, S, cq, out, out_cq, out_q0, nb);
+  ::mdp::launch_k(maxpool_kernel, bx, 256, 0, st, in, in_cq, S, cq, out, out_cq, out_q0, nb);
   MDP_LAUNCH_CHECK("maxpool_kernel");
   return MDP_OK;
 }
@@ -325,7 +331,7 @@ static int launch_tconv(int nb, const float4* in, int in_cq, int cin, int cout, 
     npad = npad > 64 ? 64 : npad;
   }
   dim3 grid(nmain + npad, 8 * (cout / 16), nb);
-  tconv_kernel<<<grid, 128, 0, st>>>(in, in_cq, cin, Sin, op, w, bias, out, out_cq, out_q0, round_tf32, nmain);
+  ::mdp::launch_k(tconv_kernel, grid, 128, 0, st, in, in_cq, cin, Sin, op, w, bias, out, out_cq, out_q0, round_tf32, nmain);
   MDP_LAUNCH_CHECK("tconv_kernel");
   return MDP_OK;
 }
@@ -426,10 +432,10 @@ extern "C" int mdp_unet_apply(const mdp_unet* net, int32_t nb, const int32_t* se
   {
     int bx = ceil_div(N, 256);
     bx = bx > 8 * sm_count() ? 8 * sm_count() : bx;
-    pack_input_kernel<<<dim3(bx, nb), 256, 0, st>>>(sel, r, ld, rnorm, dist, ldd, xin, N);
+    ::mdp::launch_k(pack_input_kernel, dim3(bx, nb), 256, 0, st, sel, r, ld, rnorm, dist, ldd, xin, N);
     MDP_LAUNCH_CHECK("pack_input_kernel");
   }
-  enc1a_kernel<<<dim3(ceil_div((int64_t)((n + 1) / 2) * n * n, 128), nb), 128, 0, st>>>(xin, n, net->w[0], net->b[0],
+  ::mdp::launch_k(enc1a_kernel, dim3(ceil_div((int64_t)((n + 1) / 2) * n * n, 128), nb), 128, 0, st, xin, n, net->w[0], net->b[0],
                                                                                        a1, tf);
   MDP_LAUNCH_CHECK("enc1a_kernel");
 
@@ -464,7 +470,7 @@ extern "C" int mdp_unet_apply(const mdp_unet* net, int32_t nb, const int32_t* se
     return tc_conv3(nb, n, 64, 32, c1, 16, 0, net->w[8], net->b[8], 1, nullptr, 0, 0, EPI_HEAD, &H, ws + P.o_scr,
                     P.scr_bytes, st);
   }
-  head_kernel<<<dim3(ceil_div(N, 128), nb), 128, 0, st>>>(d1, n, net->w[9], net->b[9], net->w[10], net->b[10],
+  ::mdp::launch_k(head_kernel, dim3(ceil_div(N, 128), nb), 128, 0, st, d1, n, net->w[9], net->b[9], net->w[10], net->b[10],
                                                           sel, rnorm, z, ldz, net->accumulate);
   MDP_LAUNCH_CHECK("head_kernel");
   return MDP_OK;

@@ -264,6 +264,8 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
+  // prologue (barriers, TMEM, tensor-map prefetch) overlapped with the previous grid
+  MDP_PDL_ENTER();
   const int nunits = A.fold ? 9 : 27;
 
   if (warp == 3) {
@@ -508,6 +510,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
 __global__ void conv_split_reduce_kernel(const float4* __restrict__ part, int ksplit, int nb, int cq, int S,
                                          const float* __restrict__ bias, int relu, int pool, float4* __restrict__ out,
                                          int out_cq, int out_q0) {
+  MDP_PDL_ENTER();
   const int So = pool ? S / 2 : S;
   const int64_t S3 = (int64_t)S * S * S, So3 = (int64_t)So * So * So;
   const int64_t total = (int64_t)nb * cq * So3;
@@ -541,6 +544,7 @@ __global__ void conv_split_reduce_kernel(const float4* __restrict__ part, int ks
 // one voxel + bias + ReLU + TF32 rounding, then the heads and ||r|| scaling.
 __global__ void conv_split_reduce_head_kernel(const float4* __restrict__ part, int ksplit, int nb, int S,
                                               const float* __restrict__ bias, int relu, const HeadArgs H) {
+  MDP_PDL_ENTER();
   const int64_t S3 = (int64_t)S * S * S;
   const int64_t total = (int64_t)nb * S3;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -590,6 +594,7 @@ struct TconvArgs {
 };
 
 __global__ void __launch_bounds__(128, 1) tconv_tc_kernel(const TconvArgs T) {
+  MDP_PDL_ENTER();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int b = blockIdx.z, grp = blockIdx.y;
   if ((int)blockIdx.x >= T.nmain) {  // tail blocks: output-padding planes
@@ -848,15 +853,15 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   MDP_REQUIRE(smem <= 227 * 1024, "tc conv needs %zu bytes of shared memory", smem);
   int grid = A.ntiles < sm_count() ? A.ntiles : sm_count();
   if (zp == 4)
-    conv3_tc_kernel<4><<<grid, 256, smem, st>>>(map, wmap, A);
+    ::mdp::launch_k(conv3_tc_kernel<4>, grid, 256, smem, st, map, wmap, A);
   else
-    conv3_tc_kernel<2><<<grid, 256, smem, st>>>(map, wmap, A);
+    ::mdp::launch_k(conv3_tc_kernel<2>, grid, 256, smem, st, map, wmap, A);
   MDP_LAUNCH_CHECK("conv3_tc_kernel");
   if (A.ksplit > 1 && epi == EPI_HEAD) {
     const int64_t total = (int64_t)nb * S * S * S;
     int bx = ceil_div(total, 128);
     bx = bx > 8 * sm_count() ? 8 * sm_count() : bx;
-    conv_split_reduce_head_kernel<<<bx, 128, 0, st>>>(A.partial, A.ksplit, nb, S, bias, relu, A.head);
+    ::mdp::launch_k(conv_split_reduce_head_kernel, bx, 128, 0, st, A.partial, A.ksplit, nb, S, bias, relu, A.head);
     MDP_LAUNCH_CHECK("conv_split_reduce_head_kernel");
   } else if (A.ksplit > 1) {
     const int pool = epi == EPI_POOL;
@@ -864,7 +869,7 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
     const int64_t total = (int64_t)nb * (cout / 4) * So * So * So;
     int bx = ceil_div(total, 256);
     bx = bx > 4 * sm_count() ? 4 * sm_count() : bx;
-    conv_split_reduce_kernel<<<bx, 256, 0, st>>>(A.partial, A.ksplit, nb, cout / 4, S, bias, relu, pool, out,
+    ::mdp::launch_k(conv_split_reduce_kernel, bx, 256, 0, st, A.partial, A.ksplit, nb, cout / 4, S, bias, relu, pool, out,
                                                  out_cq, out_q0);
     MDP_LAUNCH_CHECK("conv_split_reduce_kernel");
   }
@@ -916,7 +921,7 @@ int tc_tconv(int nb, const float4* in, int in_cq, int cin, int cout, int Sin, in
     attr_set = 227 * 1024;
   }
   dim3 grid(T.nmain + npad, 8 / tg, nb);
-  tconv_tc_kernel<<<grid, 128, smem, st>>>(T);
+  ::mdp::launch_k(tconv_tc_kernel, grid, 128, smem, st, T);
   MDP_LAUNCH_CHECK("tconv_tc_kernel");
   return MDP_OK;
 }
