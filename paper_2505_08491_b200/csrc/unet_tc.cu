@@ -576,16 +576,16 @@ __global__ void conv_split_reduce_head_kernel(const float4* __restrict__ part, i
 // ---------------------------------------------------------------------------
 // Transposed conv k=2 s=2 (neural.py:215-246) as tcgen05 GEMMs: every output
 // voxel takes exactly one tap, so per tap it is [input voxels x Cin] x [Cin x
-// Cout].  CTA = 128 consecutive input voxels (one M=128 block) x a group of
-// tg taps: the voxels' Cin channels (cin/4 quad rows of 2 KB, 1-D bulk
-// copies, K-major core matrices of 8 voxels x 16 B) and the group's weights
-// ([tap][quad][Cout][4]) land in shared memory once; one MMA chain per tap
-// accumulates into its own TMEM columns; the four warps then read their 32
-// TMEM lanes and scatter each tap's row to output voxel (2x+a, 2y+b, 2z+c).
-// Tail blocks write the output-padding planes.
+// Cout].  Persistent CTAs, one group of tg taps each: the group's weights
+// ([tap][quad][Cout][4]) are loaded once; a producer warp streams 128-voxel
+// M-tiles (cin/4 quad rows of 2 KB, 1-D bulk copies, already K-major core
+// matrices of 8 voxels x 16 B) into a double buffer; one thread issues a
+// K-chain per tap into the tile's TMEM buffer (double-buffered); four
+// epilogue warps scatter each tap's row to output voxel (2x+a, 2y+b, 2z+c)
+// while the next tile's MMAs run.  Tail blocks write the output-padding planes.
 struct TconvArgs {
   const float4* in;
-  int in_cq, cin, cout, Sin, op, tg, nmain;
+  int in_cq, cin, cout, Sin, op, tg, nmain, nb, ntiles, ncta;
   const float* w;
   const float* bias;
   float4* out;
@@ -593,32 +593,39 @@ struct TconvArgs {
   uint32_t a_bytes, b_bytes, tmem_cols;
 };
 
-__global__ void __launch_bounds__(128, 1) tconv_tc_kernel(const TconvArgs T) {
+__global__ void __launch_bounds__(192, 1) tconv_tc_kernel(const TconvArgs T) {
   MDP_PDL_ENTER();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const int b = blockIdx.z, grp = blockIdx.y;
-  if ((int)blockIdx.x >= T.nmain) {  // tail blocks: output-padding planes
+  const int grp = blockIdx.y;
+  if ((int)blockIdx.x >= T.ncta) {  // tail blocks: output-padding planes
     if (grp == 0)
-      tconv_pad(T.Sin, T.cout, T.bias, T.out, T.out_cq, T.out_q0, b,
-                (blockIdx.x - T.nmain) * (int64_t)blockDim.x + threadIdx.x,
-                (int64_t)(gridDim.x - T.nmain) * blockDim.x, 1);
+      for (int b = 0; b < T.nb; ++b)
+        tconv_pad(T.Sin, T.cout, T.bias, T.out, T.out_cq, T.out_q0, b,
+                  (blockIdx.x - T.ncta) * (int64_t)blockDim.x + threadIdx.x,
+                  (int64_t)(gridDim.x - T.ncta) * blockDim.x, 1);
     return;
   }
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sA = smem;
-  uint8_t* sB = sA + T.a_bytes;
-  uint64_t* full = (uint64_t*)(sB + T.b_bytes);
-  uint64_t* done = full + 1;
-  uint32_t* tmem_slot = (uint32_t*)(done + 1);
+  uint8_t* sB = smem;
+  uint8_t* sA = sB + T.b_bytes;  // two A buffers
+  uint64_t* bfull = (uint64_t*)(sA + 2 * (size_t)T.a_bytes);
+  uint64_t* afull = bfull + 1;
+  uint64_t* aempty = afull + 2;
+  uint64_t* tfull = aempty + 2;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Sin = T.Sin;
   const int64_t nvi = (int64_t)Sin * Sin * Sin;
-  const int64_t v0 = (int64_t)blockIdx.x * 128;
-  const int nvox = (int)(nvi - v0 < 128 ? nvi - v0 : 128);
   const int nq = T.cin / 4;
   if (threadIdx.x == 0) {
-    mbar_init(full, 1);
-    mbar_init(done, 1);
+    mbar_init(bfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&afull[i], 1);
+      mbar_init(&aempty[i], 1);
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -630,56 +637,89 @@ __global__ void __launch_bounds__(128, 1) tconv_tc_kernel(const TconvArgs T) {
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) {
-    const uint32_t rowb = (uint32_t)nvox * 16u;
-    mbar_expect_tx(full, rowb * nq + T.b_bytes);
-    for (int q = 0; q < nq; ++q)
-      bulk_load(sA + (size_t)q * 2048, T.in + ((int64_t)b * T.in_cq + q) * nvi + v0, rowb, full);
-    bulk_load(sB, T.w + (size_t)grp * T.tg * T.cin * T.cout, T.b_bytes, full);
-    mbar_wait(full, 0);
-    fence_after();
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(T.cout >> 3) << 17) |
-                           ((uint32_t)(128 >> 4) << 24);
-    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-    for (int t = 0; t < T.tg; ++t)
-      for (int ks = 0; ks < nq / 2; ++ks) {
-        const uint64_t ad = umma_desc(a0 + ks * 2 * 2048, 2048, 128);
-        const uint64_t bd = umma_desc(b0 + (uint32_t)((t * nq + 2 * ks) * T.cout * 16), T.cout * 16, 128);
-        mma_tf32(tmem + (uint32_t)(t * T.cout), ad, bd, idesc, ks > 0 ? 1u : 0u);
+  const uint32_t tstride = (uint32_t)(T.tg * T.cout);  // TMEM columns per tile buffer
+  if (warp == 0) {
+    if (lane == 0) {  // ---- producer: weights once, then the voxel rows of each tile
+      mbar_expect_tx(bfull, T.b_bytes);
+      bulk_load(sB, T.w + (size_t)grp * T.tg * T.cin * T.cout, T.b_bytes, bfull);
+      int it = 0;
+      for (int tile = blockIdx.x; tile < T.ntiles; tile += T.ncta, ++it) {
+        const int buf = it & 1;
+        mbar_wait(&aempty[buf], ((it >> 1) & 1) ^ 1);
+        const int b = tile / T.nmain;
+        const int64_t v0 = (int64_t)(tile % T.nmain) * 128;
+        const uint32_t rowb = (uint32_t)(nvi - v0 < 128 ? nvi - v0 : 128) * 16u;
+        mbar_expect_tx(&afull[buf], rowb * nq);
+        uint8_t* dst = sA + (size_t)buf * T.a_bytes;
+        for (int q = 0; q < nq; ++q)
+          bulk_load(dst + (size_t)q * 2048, T.in + ((int64_t)b * T.in_cq + q) * nvi + v0, rowb, &afull[buf]);
       }
-    mma_commit(done);
-  }
-  __syncwarp();
-  mbar_wait(done, 0);
-  fence_after();
-  // epilogue: warp w owns TMEM lanes (= voxel rows) 32w..32w+31
-  const int row = warp * 32 + lane;
-  const int64_t v = v0 + row;
-  const bool live = row < nvox;
-  const int x = live ? (int)(v % Sin) : 0, y = live ? (int)((v / Sin) % Sin) : 0,
-            z = live ? (int)(v / ((int64_t)Sin * Sin)) : 0;
-  const int So = 2 * Sin + T.op;
-  const int64_t nvo = (int64_t)So * So * So;
-  const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
-  for (int t = 0; t < T.tg; ++t) {
-    const int tap = grp * T.tg + t;
-    const int64_t o = ((int64_t)(2 * z + (tap >> 2)) * So + 2 * y + ((tap >> 1) & 1)) * So + 2 * x + (tap & 1);
-    for (int cg = 0; cg < T.cout / 16; ++cg) {
-      float r[16];
-      tmem_ld16(tmem + lane_addr + (uint32_t)(t * T.cout + cg * 16), r);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        float m = r[i];
-        if (T.bias) m += T.bias[cg * 16 + i];
-        r[i] = tf32_round(fmaxf(m, 0.f));
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(T.cout >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+      const uint32_t b0 = smem_u32(sB);
+      mbar_wait(bfull, 0);
+      int it = 0;
+      for (int tile = blockIdx.x; tile < T.ntiles; tile += T.ncta, ++it) {
+        const int buf = it & 1;
+        mbar_wait(&afull[buf], (it >> 1) & 1);
+        mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
+        fence_after();
+        const uint32_t a0 = smem_u32(sA + (size_t)buf * T.a_bytes);
+        const uint32_t d0 = tmem + (uint32_t)buf * tstride;
+        for (int t = 0; t < T.tg; ++t)
+          for (int ks = 0; ks < nq / 2; ++ks) {
+            const uint64_t ad = umma_desc(a0 + ks * 2 * 2048, 2048, 128);
+            const uint64_t bd = umma_desc(b0 + (uint32_t)((t * nq + 2 * ks) * T.cout * 16), T.cout * 16, 128);
+            mma_tf32(d0 + (uint32_t)(t * T.cout), ad, bd, idesc, ks > 0 ? 1u : 0u);
+          }
+        mma_commit(&aempty[buf]);  // voxel rows reusable once these MMAs have read them
+        mma_commit(&tfull[buf]);
       }
-      if (live)
+    }
+  } else {  // ---- epilogue warps 2..5: TMEM lanes 32 (warp % 4) ..
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
+    const int So = 2 * Sin + T.op;
+    const int64_t nvo = (int64_t)So * So * So;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < T.ntiles; tile += T.ncta, ++it) {
+      const int buf = it & 1;
+      const int b = tile / T.nmain;
+      const int64_t v = (int64_t)(tile % T.nmain) * 128 + row;
+      const bool live = v < nvi;
+      const int x = live ? (int)(v % Sin) : 0, y = live ? (int)((v / Sin) % Sin) : 0,
+                z = live ? (int)(v / ((int64_t)Sin * Sin)) : 0;
+      mbar_wait(&tfull[buf], (it >> 1) & 1);
+      fence_after();
+      const uint32_t d0 = tmem + lane_addr + (uint32_t)buf * tstride;
+      for (int t = 0; t < T.tg; ++t) {
+        const int tap = grp * T.tg + t;
+        const int64_t o = ((int64_t)(2 * z + (tap >> 2)) * So + 2 * y + ((tap >> 1) & 1)) * So + 2 * x + (tap & 1);
+        for (int cg = 0; cg < T.cout / 16; ++cg) {
+          float r[16];
+          tmem_ld16(d0 + (uint32_t)(t * T.cout + cg * 16), r);
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          T.out[((int64_t)b * T.out_cq + T.out_q0 + cg * 4 + q) * nvo + o] =
-              make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+          for (int i = 0; i < 16; ++i) {
+            float m = r[i];
+            if (T.bias) m += T.bias[cg * 16 + i];
+            r[i] = tf32_round(fmaxf(m, 0.f));
+          }
+          if (live)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              T.out[((int64_t)b * T.out_cq + T.out_q0 + cg * 4 + q) * nvo + o] =
+                  make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+        }
+      }
+      fence_before();
+      mbar_arrive(&tempty[buf]);
     }
   }
+  __syncwarp();
   fence_before();
   __syncthreads();
   fence_after();
@@ -893,35 +933,42 @@ int tc_tconv(int nb, const float4* in, int in_cq, int cin, int cout, int Sin, in
   T.out = out;
   T.out_cq = out_cq;
   T.out_q0 = out_q0;
+  T.nb = nb;
   T.a_bytes = (uint32_t)cin * 128 * 4;
+  const int64_t nvi = (int64_t)Sin * Sin * Sin;
+  T.nmain = ceil_div(nvi, 128);
+  T.ntiles = T.nmain * nb;
+  // taps per CTA: weights + two voxel-row buffers in shared memory, two TMEM
+  // tile buffers; on small grids fewer taps per CTA for parallelism
   const size_t budget = 200 * 1024;
   int tg = 8;
-  while (tg > 1 && ((size_t)T.a_bytes + (size_t)tg * cin * cout * 4 > budget || tg * cout > 256)) tg >>= 1;
-  // small grids: fewer taps per CTA (more CTAs, shorter serial MMA + epilogue chains)
-  const int64_t mt = (int64_t)ceil_div((int64_t)Sin * Sin * Sin, 128) * nb;
-  while (tg > 1 && mt * (8 / tg) < 2 * sm_count()) tg >>= 1;
+  while (tg > 1 && (2 * (size_t)T.a_bytes + (size_t)tg * cin * cout * 4 > budget || 2 * tg * cout > 512)) tg >>= 1;
+  while (tg > 1 && (int64_t)T.ntiles * (8 / tg) < 2 * sm_count()) tg >>= 1;
   T.tg = tg;
   T.b_bytes = (uint32_t)(tg * cin * cout * 4);
   uint32_t cols = 32;
-  while (cols < (uint32_t)(tg * cout)) cols <<= 1;
+  while (cols < (uint32_t)(2 * tg * cout)) cols <<= 1;
   T.tmem_cols = cols;
-  const int64_t nvi = (int64_t)Sin * Sin * Sin;
-  T.nmain = ceil_div(nvi, 128);
+  const int groups = 8 / tg;
+  int ncta = sm_count() / groups;
+  ncta = ncta < 1 ? 1 : (ncta > T.ntiles ? T.ntiles : ncta);
+  T.ncta = ncta;
   int npad = 0;
   if (op) {
     const int So = 2 * Sin + 1;
     const int64_t per_item = ((int64_t)So * So * So - 8 * nvi) * (cout / 4);
-    npad = ceil_div(per_item, 128);
+    npad = ceil_div(per_item, 192);
     npad = npad > 64 ? 64 : npad;
   }
-  const size_t smem = 1024 + (size_t)T.a_bytes + T.b_bytes + 64;
-  static size_t attr_set = 0;
-  if (attr_set < smem) {
+  const size_t smem = 1024 + (size_t)T.b_bytes + 2 * (size_t)T.a_bytes + 128;
+  MDP_REQUIRE(smem <= 227 * 1024, "tc tconv needs %zu bytes of shared memory", smem);
+  static bool attr_set = false;
+  if (!attr_set) {
     cudaFuncSetAttribute(tconv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
-    attr_set = 227 * 1024;
+    attr_set = true;
   }
-  dim3 grid(T.nmain + npad, 8 / tg, nb);
-  ::mdp::launch_k(tconv_tc_kernel, grid, 128, smem, st, T);
+  dim3 grid(ncta + npad, groups, 1);
+  ::mdp::launch_k(tconv_tc_kernel, grid, 192, smem, st, T);
   MDP_LAUNCH_CHECK("tconv_tc_kernel");
   return MDP_OK;
 }

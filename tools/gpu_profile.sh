@@ -21,8 +21,8 @@ run_full conv_enc2_33 conv3_tc_kernel 2 python tools/conv_one.py 33 32 64 1 3
 run_full conv_dec1_129 conv3_tc_kernel 2 python tools/conv_one.py 129 64 32 0 3
 run_full conv_enc2_129 conv3_tc_kernel 2 python tools/conv_one.py 129 32 64 1 3
 run_full conv_enc3_65 conv3_tc_kernel 2 python tools/conv_one.py 65 64 128 1 3
-run_full stencil_129x8 stencil_kernel 4 python tools/spmv_one.py 129 8 3 coupled
-run_full stencil_33 stencil_kernel 4 python tools/spmv_one.py 33 1 3 coupled
+run_full stencil_129x8 stencil_kernel 1 python tools/spmv_one.py 129 8 3 coupled
+run_full stencil_33 stencil_kernel 1 python tools/spmv_one.py 33 1 3 coupled
 run_full tconv_129 tconv_tc_kernel 3 python tools/cnn_one.py 129 1 2
 timeout 600 python tools/step_breakdown.py --maxit 60 --out $O/breakdown_cfg2.json > $O/breakdown_cfg2.log 2>&1
 for cfg in "129 1" "65 16" "33 1"; do set -- $cfg; timeout 300 python tools/cnn_breakdown.py --n $1 --nb $2 --out $O/cnn_$1_$2.json > /dev/null 2>&1; done
