@@ -40,12 +40,13 @@ inline int check_launch(const char* what) {
 
 __device__ __forceinline__ int sys_of(const int32_t* sel, int i) { return sel ? sel[i] : i; }
 
-// Programmatic dependent launch: every kernel is launched with programmatic
-// stream serialisation (also inside captured CUDA graphs), so the next grid
-// is scheduled while this one drains.  Each kernel enters with
-// MDP_PDL_ENTER(): wait until the preceding grid has completed and its memory
-// is visible, then allow the following grid to launch.  Nothing touches
-// global memory before the wait, so the ordering is the plain stream order.
+// Programmatic dependent launch (opt-in, MDP_PDL=1): kernels are launched
+// with programmatic stream serialisation (also inside captured CUDA graphs),
+// so the next grid is scheduled while this one drains.  Each kernel enters
+// with MDP_PDL_ENTER(): wait until the preceding grid has completed and its
+// memory is visible, then allow the following grid to launch (both are
+// no-ops for a normal launch).  Nothing touches global memory before the
+// wait, so the ordering is the plain stream order.
 #define MDP_PDL_ENTER()                                             \
   do {                                                              \
     asm volatile("griddepcontrol.wait;" ::: "memory");              \

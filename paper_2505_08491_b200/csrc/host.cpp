@@ -34,8 +34,10 @@ void set_error(const char* fmt, ...) {
 bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
+    // opt-in: inside the solve's CUDA graphs PDL measured +0.6% at 33^3 but
+    // eager 129^3 CNN forwards lost 10% (profiles/r01_pdl_ab.txt)
     const char* e = getenv("MDP_PDL");
-    on = e ? atoi(e) != 0 : 1;
+    on = e ? atoi(e) != 0 : 0;
   }
   return on != 0;
 }
