@@ -8,6 +8,12 @@ FLOPs per SURVEY.md section 8d; peaks from MEASURED_PEAKS.json (HBM) and a
 cuBLAS TF32 GEMM measured in the same run.
 
     python tools/bench_ops.py [--sizes 33,65,129,193] [--batches 1,8,64] [--out f.json]
+                              [--cpu-sizes 33,65,129] [--cpu-cnn-max 65]
+
+--cpu-sizes: also time the CPU oracle (the reference path restated in
+numpy/scipy, same seeded batch-1 system) per operator on the host cores:
+full_operator @ x, T @ x3, T^T v, a 30-vector MGS step (krylov.py:138-140)
+and the U-Net forward (n <= --cpu-cnn-max).
 """
 
 from __future__ import annotations
@@ -40,6 +46,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--mem-gb", type=float, default=120.0)
     ap.add_argument("--out", default="")
+    ap.add_argument("--cpu-sizes", default="")
+    ap.add_argument("--cpu-cnn-max", type=int, default=65)
     a = ap.parse_args()
     lib = _ext.lib()
     pk = bench.peaks()
@@ -71,7 +79,7 @@ def main():
             ms = timed(lambda: A.matvec(X, Y), a.reps, flush)
             byt = sum(16 * x for x in N) + 40 * Q
             r["spmv"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9, "frac_hbm": byt / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
-                         "bytes": byt}
+                         "frac_hbm_spec_8tbs": byt / (ms * 1e-3) / 8e12, "bytes": byt}
             S = torch.zeros(max(Q, 1), dtype=torch.float64, device="cuda")
             ms = timed(lambda: ops.gather(X, None, S), a.reps, flush)
             byt = 112 * Q
@@ -113,9 +121,56 @@ def main():
             print(json.dumps(r), flush=True)
             del prob, A, ops, X, Y, S, D, Z, R
             torch.cuda.empty_cache()
-    out = {"peaks": pk, "tf32_tflops_measured": tf32, "rows": rows}
+    cpu = [cpu_row(int(n), a.cpu_cnn_max) for n in a.cpu_sizes.split(",") if n]
+    out = {"peaks": pk, "tf32_tflops_measured": tf32, "rows": rows, "cpu_oracle": cpu}
     if a.out:
         Path(a.out).write_text(json.dumps(out, indent=1))
+
+
+def cpu_row(n: int, cnn_max: int) -> dict:
+    """The CPU oracle's per-operator times for the batch-1 cfg5 system at n (median of reps)."""
+    import os
+    import statistics
+    import oracle
+    from oracle import problem as OP
+
+    def t(fn, reps):
+        fn()  # warm (first calls pay allocation / BLAS start-up)
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts) * 1e3
+
+    R = min(0.005, 0.9 / (n - 1))
+    t0 = time.perf_counter()
+    o = OP.assemble_coupled_system(OP.StructuredGrid(n), OP.random_tree(32, 4000, R),
+                                   OP.PhysicalParams(epsilon=R, beta=1.0), n_circle=8, elems_per_edge=16,
+                                   bc3d="dirichlet", f1d=1.0)
+    A = OP.full_operator(o)
+    T = o.restriction.matrix
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(A.shape[0])
+    v = rng.standard_normal(T.shape[0])
+    V = rng.standard_normal((30, A.shape[0]))
+
+    def mgs():  # krylov.py:138-140 for one Arnoldi step against 30 basis vectors
+        w = x.copy()
+        for i in range(30):
+            h = float(w @ V[i])
+            w -= h * V[i]
+        return np.linalg.norm(w)
+
+    row = {"n": n, "cores": len(os.sched_getaffinity(0)), "assembly_s": round(time.perf_counter() - t0, 2),
+           "spmv_ms": t(lambda: A @ x, 5), "pi_gather_ms": t(lambda: T @ x[:o.n3], 5),
+           "pi_scatter_ms": t(lambda: T.T @ v, 5), "mgs30_ms": t(mgs, 3)}
+    if n <= cnn_max:
+        xin = rng.standard_normal((1, 2, n, n, n))
+        p = oracle.noisy_params(4)
+        row["cnn_forward_ms"] = t(lambda: oracle.unet_forward(p, xin), 1)
+    print(json.dumps({"cpu_oracle": row}), flush=True)
+    return row
 
 
 def neural_flops(n: int) -> float:
