@@ -234,6 +234,7 @@ def target_128(tf32_peak, hbm_peak):
                         "note": "pack + 9 conv/tconv layers + heads; flops per SURVEY.md 8d"},
         "spmv": {"bound": "hbm", "ms": sp_ms, "bytes": sp_bytes, "achieved": sp_bytes / (sp_ms * 1e-3) / 1e9,
                  "peak": hbm_peak, "unit": "GB/s", "frac": sp_bytes / (sp_ms * 1e-3) / 1e9 / hbm_peak,
+                 "frac_of_8tbs_spec": sp_bytes / (sp_ms * 1e-3) / 8e12,
                  "note": "L2 flushed before every rep"},
     }
     del prob, A, X, Y, flush, net
@@ -430,6 +431,7 @@ def run_ours(args):
             "roofline_spmv": {"bound": "hbm", "kernel": "coupled SpMV (stencil+Pi)",
                               "achieved": spmv_bytes / (spmv_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"],
                               "unit": "GB/s", "frac": spmv_bytes / (spmv_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                              "frac_of_8tbs_spec": spmv_bytes / (spmv_ms * 1e-3) / 8e12,
                               "note": "L2-resident at this size" if spmv_bytes < 2 * 126e6 else ""},
             "e2e": {"value": len(wl.systems) / (e2e_ms * 1e-3), "unit": "solves/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
