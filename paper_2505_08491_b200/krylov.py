@@ -76,10 +76,13 @@ class _State:
         self.done = False
         self.r0 = 0.0
         self.hist = [1.0]
-        self.H = np.zeros((k + 1, k))
-        self.cs = np.zeros(k)
-        self.sn = np.zeros(k)
-        self.g = np.zeros(k + 1)
+        # Hessenberg columns (rotated) and Givens state as Python floats: the
+        # per-step host work runs while the device idles, and float ops are
+        # the same IEEE double ops as numpy scalars (krylov.py:142-157)
+        self.H = []
+        self.cs = [0.0] * k
+        self.sn = [0.0] * k
+        self.g = [0.0] * (k + 1)
         self.rel = 0.0
         self.beta = 0.0
 
@@ -268,10 +271,10 @@ class FgmresEngine:
                         self._finish(S)
                         continue
                     go.append(s)
-                    S.H[:] = 0.0
-                    S.cs[:] = 0.0
-                    S.sn[:] = 0.0
-                    S.g[:] = 0.0
+                    S.H = []
+                    S.cs = [0.0] * k
+                    S.sn = [0.0] * k
+                    S.g = [0.0] * (k + 1)
                     S.g[0] = S.beta
                     S.j = 0
                 if go:
@@ -329,22 +332,23 @@ class FgmresEngine:
             for i, s in enumerate(arn):
                 S = st[s]
                 j = S.j
-                H, cs, sn, g = S.H, S.cs, S.sn, S.g
-                H[:j + 1, j] = hc[i, :j + 1]
+                cs, sn, g = S.cs, S.sn, S.g
+                col = hc[i, :j + 1].tolist()
                 h_next = float(hc[i, k + 1])
                 for ii in range(j):
-                    t = cs[ii] * H[ii, j] + sn[ii] * H[ii + 1, j]
-                    H[ii + 1, j] = -sn[ii] * H[ii, j] + cs[ii] * H[ii + 1, j]
-                    H[ii, j] = t
-                denom = np.hypot(H[j, j], h_next)
+                    a, c = col[ii], col[ii + 1]
+                    col[ii + 1] = -sn[ii] * a + cs[ii] * c
+                    col[ii] = cs[ii] * a + sn[ii] * c
+                denom = float(np.hypot(col[j], h_next))
                 if denom < BREAKDOWN_TOL:
                     S.iters += 1
                     S.hist.append(S.hist[-1])
                     S.brk += 1
                     ending.append(s)
                     continue
-                cs[j], sn[j] = H[j, j] / denom, h_next / denom
-                H[j, j] = denom
+                cs[j], sn[j] = col[j] / denom, h_next / denom
+                col[j] = denom
+                S.H.append(col)
                 g[j + 1] = -sn[j] * g[j]
                 g[j] = cs[j] * g[j]
                 S.iters += 1
@@ -383,9 +387,13 @@ class FgmresEngine:
             for i, s in enumerate(upd):
                 S = st[s]
                 j = S.j
+                Hm = np.zeros((j, j))  # upper triangle of the rotated Hessenberg (krylov.py:168-171)
+                for c in range(j):
+                    Hm[:c + 1, c] = S.H[c][:c + 1]
+                g = np.asarray(S.g)
                 y = np.zeros(j)
                 for ii in range(j - 1, -1, -1):
-                    y[ii] = (S.g[ii] - S.H[ii, ii + 1:j] @ y[ii + 1:j]) / S.H[ii, ii]
+                    y[ii] = (g[ii] - Hm[ii, ii + 1:j] @ y[ii + 1:j]) / Hm[ii, ii]
                 ys[i, :j] = y
             sel = self._upload("end", upd)
             cnt = self._upload("cnt", [st[s].j for s in upd])
