@@ -64,7 +64,6 @@ struct ConvArgs {
   int resident;  // 1: the whole filter (27 taps, one chunk) stays in shared memory
   int tps;       // taps (fold: (dy,dx) units) per weight stage (one mbarrier handshake per stage)
   int fold;      // Cout == 32: the 3 z-taps of one (dy,dx) are one N = 3*32 weight block (see issue_stage_fold)
-  int dbg;       // MDP_DEBUG_CONV bits (timing experiments only): 1 no stores, 2 no MMA, 4 no TMA, 8 no weight copies
   uint32_t tmem_cols;
   HeadArgs head;
 };
@@ -276,14 +275,10 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
         decode_tile<ZP>(A, tile, b, x0, y0, z0, n0, ks);
         for (int c = ks * A.cps; c < (ks + 1) * A.cps; ++c) {
           mbar_wait(&a_empty[as], ap ^ 1);
-          if (A.dbg & 4) {
-            mbar_arrive(&a_full[as]);
-          } else {
-            mbar_expect_tx(&a_full[as], A.a_bytes);
-            // inner box row = 10 voxels x 4 channels (160 B); coordinate -4 floats = voxel x0-1
-            tma_load_4d(sA + (size_t)as * A.a_bytes, &tmap, &a_full[as], 4 * (x0 - 1), y0 - 1, z0 - 1,
-                        b * A.in_cq + A.in_q0 + c * A.cqc);
-          }
+          mbar_expect_tx(&a_full[as], A.a_bytes);
+          // inner box row = 10 voxels x 4 channels (160 B); coordinate -4 floats = voxel x0-1
+          tma_load_4d(sA + (size_t)as * A.a_bytes, &tmap, &a_full[as], 4 * (x0 - 1), y0 - 1, z0 - 1,
+                      b * A.in_cq + A.in_q0 + c * A.cqc);
           if (++as == A.na) { as = 0; ap ^= 1; }
         }
       }
@@ -303,11 +298,6 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           const float* wc = A.w + (size_t)c * nunits * tap_floats;
           for (int t0 = 0; t0 < nunits; t0 += A.tps) {
             mbar_wait(&b_empty[bs], bp ^ 1);
-            if (A.dbg & 8) {
-              mbar_arrive(&b_full[bs]);
-              if (++bs == A.nbs) { bs = 0; bp ^= 1; }
-              continue;
-            }
             mbar_expect_tx(&b_full[bs], A.b_bytes);
             uint8_t* dst = sB + (size_t)bs * A.b_bytes;
             const float* src = wc + (size_t)t0 * tap_floats;
@@ -354,13 +344,13 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
             const uint32_t b_lo = (uint32_t)bd0, b_hi = (uint32_t)(bd0 >> 32);
             const uint32_t b_tap16 = (uint32_t)(A.cqc * A.ncol * (A.fold ? 3 : 1));  // one unit's weights / 16 B
             const uint32_t b_ks16 = (uint32_t)(2 * A.ncol * (A.fold ? 3 : 1));         // (2 * lbo_b) / 16
-            if (!(A.dbg & 2) && A.fold) {
+            if (A.fold) {
               switch (A.tps) {
                 case 9: issue_stage_fold<9, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc_n, accf); break;
                 case 3: issue_stage_fold<3, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc_n, accf); break;
                 default: issue_stage_fold<1, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc_n, accf); break;
               }
-            } else if (!(A.dbg & 2)) {
+            } else {
               switch (A.tps) {
                 case 27: issue_stage<27, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
                 case 9: issue_stage<9, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc, accf); break;
@@ -405,7 +395,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           for (int cg = 0; cg < A.ncol / 16; ++cg) {
             float v[16];
             tmem_ld16(dcol + zcol(zp) + cg * 16, v);
-            if (ok && !(A.dbg & 1)) {
+            if (ok) {
 #pragma unroll
               for (int q = 0; q < 4; ++q)
                 A.partial[(((int64_t)ks * A.nb + b) * (A.cout / 4) + n0 / 4 + cg * 4 + q) * S3 +
@@ -432,7 +422,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
             if (A.relu) m = fmaxf(m, 0.f);
             v[i] = tf32_round(m);
           }
-          if (ok && !(A.dbg & 1)) {
+          if (ok) {
             const float y = head_eval(v, H.w1, H.b1, H.w2, H.b2);
             double* zp = H.z + sys * H.ldz + ((int64_t)gz * S + gy) * S + gx;
             *zp = H.accumulate ? *zp + rn * (double)y : rn * (double)y;
@@ -457,7 +447,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
               if (A.relu) m = fmaxf(m, 0.f);
               v0[i] = tf32_round(m);
             }
-            if (writer && !(A.dbg & 1)) {
+            if (writer) {
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 float4 o = make_float4(v0[4 * q], v0[4 * q + 1], v0[4 * q + 2], v0[4 * q + 3]);
@@ -481,7 +471,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
               if (A.relu) m = fmaxf(m, 0.f);
               v[i] = tf32_round(m);
             }
-            if (ok && !(A.dbg & 1)) {
+            if (ok) {
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -756,8 +746,14 @@ static void tc_split(int nb, int S, int cin, int cout, int& nsplit, int& ksplit)
   int nsplit_item = 1;
   while (tiles_item * nsplit_item < sm_count() && cout / (2 * nsplit_item) >= 32) nsplit_item *= 2;
   ksplit = 1;
-  const int want = (sm_count() + tiles_item * nsplit_item - 1) / (tiles_item * nsplit_item);
-  if (tiles_item * nsplit_item * 2 <= sm_count())
+#ifndef CONV_SPLITK
+#define CONV_SPLITK 1
+#endif
+#ifndef CONV_SPLITK_WAVES
+#define CONV_SPLITK_WAVES 1  // target CTAs = waves x SMs
+#endif
+  const int want = (CONV_SPLITK_WAVES * sm_count() + tiles_item * nsplit_item - 1) / (tiles_item * nsplit_item);
+  if (CONV_SPLITK && tiles_item * nsplit_item * 2 <= sm_count())
     for (int k = nchunk; k >= 2; --k)
       if (nchunk % k == 0 && k <= want) {
         ksplit = k;
@@ -846,14 +842,6 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   MDP_REQUIRE(cols <= 512, "conv accumulators need %u TMEM columns", cols);
   A.tmem_cols = cols;
   if (head) A.head = *head;
-  {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* e = getenv("MDP_DEBUG_CONV");
-      dbg = e ? atoi(e) : 0;
-    }
-    A.dbg = dbg;
-  }
 
   // 4-D view of the quad-blocked activations: (x * 4 + channel, y, z, item * CQ + quad);
   // the innermost box row is a whole 10-voxel x-run (160 B) of one quad
