@@ -372,7 +372,7 @@ static int launch_stencil(const mdp_problem* p, int32_t nsel, const int32_t* sel
   int zch = ceil_div(want, warps * nsel);
   // (latency-bound small grids: 2-plane chunks measured 3% faster in-solve at 33^3)
   const int zmin_len = warps * nsel * (n / 16) >= want ? 16 : (n <= 48 ? 2 : 4);
-  const int zmax = n / zmin_len > 1 ? n / zmin_len : 1;
+  const int zmax = n <= 48 ? ceil_div(n, zmin_len) : (n / zmin_len > 1 ? n / zmin_len : 1);
   zch = zch < 1 ? 1 : (zch > zmax ? zmax : zch);
   int zchunk = ceil_div(n, zch);
   {
