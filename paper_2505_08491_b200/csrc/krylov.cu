@@ -24,8 +24,12 @@ enum OrthMode { DOT = 0, UPD_DOT = 1, UPD_NORM = 2, NORM = 3 };
 #define ORTH_KB 8
 #endif
 
+#ifndef ORTH_ELEMS
+#define ORTH_ELEMS 256  // elements per reduction block before the ORTH_CAP x SMs cap (256 vs 512: -2.5% cfg2 solve)
+#endif
+
 inline int red_blocks(int64_t n) {
-  int nb = ceil_div(n, 512);
+  int nb = ceil_div(n, ORTH_ELEMS);
   int cap = ORTH_CAP * sm_count();
   return nb < 1 ? 1 : (nb > cap ? cap : nb);
 }
