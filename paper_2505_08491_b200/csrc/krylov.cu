@@ -399,40 +399,58 @@ __global__ void __launch_bounds__(256) ilu0_apply_kernel(const mdp_ilu F, const 
   const int s = sys_of(sel, blockIdx.x);
   const int rs = F.row_start[s], nrow = F.row_start[s + 1] - rs;
   const int p0 = F.ptr[rs], nnz = F.ptr[rs + nrow] - p0;
+  const int nlf = F.nlev_f[s], nlb = F.nlev_b[s];
+  const double* val = F.val + p0;
+  const int* col = F.col + p0;
+  const int* levf = F.lev_f + (int64_t)s * F.lev_stride;  // nlev+1 boundaries
+  const int* levb = F.lev_b + (int64_t)s * F.lev_stride;
+  const int* pf = F.perm_f + rs;
+  const int* pb = F.perm_b + rs;
+  const double* rp = r + s * ld;
+  // staged: the whole factor, the level schedule and r live in shared memory,
+  // so each level costs a barrier plus shared-memory latency only
   double* vsh = xsh + nrow;
   int* csh = (int*)(vsh + (staged ? nnz : 0));
   int* psh = csh + (staged ? nnz : 0);
   int* dsh = psh + (staged ? nrow + 1 : 0);
-  const double* val = F.val + p0;
-  const int* col = F.col + p0;
+  int* pfs = dsh + (staged ? nrow : 0);
+  int* pbs = pfs + (staged ? nrow : 0);
+  int* lfs = pbs + (staged ? nrow : 0);
+  int* lbs = lfs + (staged ? nlf + 1 : 0);
   if (staged) {
     for (int t = threadIdx.x; t < nnz; t += blockDim.x) {
       vsh[t] = val[t];
       csh[t] = col[t];
     }
     for (int t = threadIdx.x; t <= nrow; t += blockDim.x) psh[t] = F.ptr[rs + t] - p0;
-    for (int t = threadIdx.x; t < nrow; t += blockDim.x) dsh[t] = F.diag[rs + t] - p0;
+    for (int t = threadIdx.x; t < nrow; t += blockDim.x) {
+      dsh[t] = F.diag[rs + t] - p0;
+      pfs[t] = pf[t];
+      pbs[t] = pb[t];
+      xsh[t] = rp[t];  // the forward sweep reads r[row] before writing xsh[row]
+    }
+    for (int t = threadIdx.x; t <= nlf; t += blockDim.x) lfs[t] = levf[t];
+    for (int t = threadIdx.x; t <= nlb; t += blockDim.x) lbs[t] = levb[t];
     val = vsh;
     col = csh;
+    levf = lfs;
+    levb = lbs;
+    pf = pfs;
+    pb = pbs;
   }
-  const double* rp = r + s * ld;
-  const int* levf = F.lev_f + (int64_t)s * F.lev_stride;  // nlev+1 boundaries
-  const int* levb = F.lev_b + (int64_t)s * F.lev_stride;
-  const int* pf = F.perm_f + rs;
-  const int* pb = F.perm_b + rs;
   __syncthreads();
-  for (int L = 0; L < F.nlev_f[s]; ++L) {
+  for (int L = 0; L < nlf; ++L) {
     for (int t = levf[L] + threadIdx.x; t < levf[L + 1]; t += blockDim.x) {
       const int row = pf[t];
       const int a = staged ? psh[row] : F.ptr[rs + row] - p0;
       const int d = staged ? dsh[row] : F.diag[rs + row] - p0;
-      double acc = rp[row];
+      double acc = staged ? xsh[row] : rp[row];
       for (int p = a; p < d; ++p) acc = __dsub_rn(acc, __dmul_rn(val[p], xsh[col[p]]));
       xsh[row] = acc;
     }
     __syncthreads();
   }
-  for (int L = 0; L < F.nlev_b[s]; ++L) {
+  for (int L = 0; L < nlb; ++L) {
     for (int t = levb[L] + threadIdx.x; t < levb[L + 1]; t += blockDim.x) {
       const int row = pb[t];
       const int d = staged ? dsh[row] : F.diag[rs + row] - p0;
@@ -738,7 +756,7 @@ extern "C" int mdp_ilu0_apply(const mdp_ilu* f, int32_t nsel, const int32_t* sel
   const size_t cap = 200 * 1024;
   const size_t base = (size_t)f->max_rows * sizeof(double);
   const size_t full = base + (size_t)f->max_nnz * (sizeof(double) + sizeof(int)) +
-                      (size_t)(2 * f->max_rows + 1) * sizeof(int);
+                      (size_t)(4 * f->max_rows + 1 + 2 * f->lev_stride) * sizeof(int);
   const int staged = full <= cap;
   MDP_REQUIRE(base <= cap, "1D block of %d rows too large for the single-CTA sweep", f->max_rows);
   static bool attr = false;

@@ -1,12 +1,5 @@
 cd $GRAFT_REPO_ROOT
 export PYTHONDONTWRITEBYTECODE=1
-timeout 600 python - <<'PY'
-import sys, json, subprocess
-for lib in ["", "tools/ab/libk_e256.so", "tools/ab/libk_e128.so", ""]:
-    code = ("import sys; sys.argv=['bench.py','--steps','3','--warmup','3','--maxit','300','--no-cpu-baseline','--no-target'];"
-            + ("from pathlib import Path; from paper_2505_08491_b200 import _ext; _ext.load_library(Path('%s'));" % lib if lib else "")
-            + "import runpy; runpy.run_path('bench.py', run_name='__main__')")
-    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True).stdout.strip().splitlines()
-    d = json.loads(out[-1]) if out else {}
-    print("bench lib=%s" % (lib or "cur"), d.get("value"), d.get("ms_per_step"), flush=True)
-PY
+timeout 900 python -m pytest tests/test_gpu_ops.py tests/test_gpu_solve.py -q 2>&1 | tail -2
+timeout 600 python tools/step_breakdown.py --maxit 60 2>/dev/null | sed -n 2,14p
+for i in 1 2; do timeout 600 python bench.py --steps 3 --warmup 3 --maxit 300 --no-cpu-baseline --no-target 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['e2e']['value'])"; done
