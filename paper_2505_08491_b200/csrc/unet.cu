@@ -33,10 +33,13 @@ __global__ void pack_input_kernel(const int32_t* sel, const double* __restrict__
 }
 
 // enc1a: 3x3x3 conv 2 -> 16, bias, ReLU (neural.py:343); w [16][2][27].
-// One thread = two x-adjacent voxels.  The weights are transposed in shared
-// memory to [tap][ch][16], so one (tap, channel) is four 16-byte broadcast
-// loads feeding 32 FMAs (a scalar load per FMA made this kernel LSU-bound);
-// the 3 x 4 neighbour columns of one z-plane are loaded before their FMAs.
+// One thread = VX x-adjacent voxels (2 on large grids: weights and neighbour
+// columns shared; 1 on small, latency-bound grids: twice the threads).  The
+// weights are transposed in shared memory to [tap][ch][16], so one (tap,
+// channel) is four 16-byte broadcast loads feeding 16 VX FMAs (a scalar load
+// per FMA made this kernel LSU-bound); the neighbour columns of one z-plane
+// are loaded before their FMAs.
+template <int VX>
 __global__ void __launch_bounds__(128) enc1a_kernel(const float2* __restrict__ xin, int S,
                                                      const float* __restrict__ w,
                                                      const float* __restrict__ bias,
@@ -52,61 +55,60 @@ __global__ void __launch_bounds__(128) enc1a_kernel(const float2* __restrict__ x
   for (int t = threadIdx.x; t < 16; t += blockDim.x) bs[t] = bias ? bias[t] : 0.f;
   __syncthreads();
   const int b = blockIdx.y;
-  const int SX = (S + 1) / 2;  // voxel pairs per x-row
+  const int SX = (S + VX - 1) / VX;  // voxel groups per x-row
   const int64_t nvox = (int64_t)S * S * S;
   const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u >= (int64_t)SX * S * S) return;
-  const int x = 2 * (int)(u % SX), y = (u / SX) % S, z = u / ((int64_t)SX * S);
-  float acc0[16], acc1[16];
+  const int x = VX * (int)(u % SX), y = (u / SX) % S, z = u / ((int64_t)SX * S);
+  float acc[VX][16];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) acc0[c] = acc1[c] = bs[c];
+  for (int k = 0; k < VX; ++k)
+#pragma unroll
+    for (int c = 0; c < 16; ++c) acc[k][c] = bs[c];
   const float2* xb = xin + b * nvox;
 #pragma unroll
   for (int dz = 0; dz < 3; ++dz) {
-    // columns x-1 .. x+2 of rows y-1 .. y+1; out-of-domain neighbours are exact
+    // columns x-1 .. x+VX of rows y-1 .. y+1; out-of-domain neighbours are exact
     // zeros (same sums as skipping the tap)
-    float2 in[3][4];
+    float2 in[3][VX + 2];
     const int zz = z + dz - 1;
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
       const int yy = y + r - 1;
       const bool rok = zz >= 0 && yy >= 0 && zz < S && yy < S;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < VX + 2; ++k) {
         const int xx = x + k - 1;
         in[r][k] = rok && xx >= 0 && xx < S ? __ldg(xb + ((int64_t)zz * S + yy) * S + xx) : make_float2(0.f, 0.f);
       }
     }
 #pragma unroll
     for (int t = 0; t < 9; ++t) {
-      const int tap = dz * 9 + t, r = t / 3, k = t % 3;
-      const float2 a0 = in[r][k], a1 = in[r][k + 1];
+      const int tap = dz * 9 + t, r = t / 3, kx = t % 3;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float4 w0 = ws4[(tap * 2 + 0) * 4 + q], w1 = ws4[(tap * 2 + 1) * 4 + q];
-        acc0[4 * q + 0] += w0.x * a0.x + w1.x * a0.y;
-        acc0[4 * q + 1] += w0.y * a0.x + w1.y * a0.y;
-        acc0[4 * q + 2] += w0.z * a0.x + w1.z * a0.y;
-        acc0[4 * q + 3] += w0.w * a0.x + w1.w * a0.y;
-        acc1[4 * q + 0] += w0.x * a1.x + w1.x * a1.y;
-        acc1[4 * q + 1] += w0.y * a1.x + w1.y * a1.y;
-        acc1[4 * q + 2] += w0.z * a1.x + w1.z * a1.y;
-        acc1[4 * q + 3] += w0.w * a1.x + w1.w * a1.y;
+#pragma unroll
+        for (int k = 0; k < VX; ++k) {
+          const float2 a = in[r][kx + k];
+          acc[k][4 * q + 0] += w0.x * a.x + w1.x * a.y;
+          acc[k][4 * q + 1] += w0.y * a.x + w1.y * a.y;
+          acc[k][4 * q + 2] += w0.z * a.x + w1.z * a.y;
+          acc[k][4 * q + 3] += w0.w * a.x + w1.w * a.y;
+        }
       }
     }
   }
   const int64_t v = ((int64_t)z * S + y) * S + x;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    float4 o = make_float4(fmaxf(acc0[4 * q], 0.f), fmaxf(acc0[4 * q + 1], 0.f), fmaxf(acc0[4 * q + 2], 0.f),
-                           fmaxf(acc0[4 * q + 3], 0.f));
-    if (round_tf32) o = tf32_round4(o);
-    out[((int64_t)b * 4 + q) * nvox + v] = o;
-    if (x + 1 < S) {
-      float4 o1 = make_float4(fmaxf(acc1[4 * q], 0.f), fmaxf(acc1[4 * q + 1], 0.f), fmaxf(acc1[4 * q + 2], 0.f),
-                              fmaxf(acc1[4 * q + 3], 0.f));
-      if (round_tf32) o1 = tf32_round4(o1);
-      out[((int64_t)b * 4 + q) * nvox + v + 1] = o1;
+  for (int k = 0; k < VX; ++k) {
+    if (x + k >= S) break;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float4 o = make_float4(fmaxf(acc[k][4 * q], 0.f), fmaxf(acc[k][4 * q + 1], 0.f), fmaxf(acc[k][4 * q + 2], 0.f),
+                             fmaxf(acc[k][4 * q + 3], 0.f));
+      if (round_tf32) o = tf32_round4(o);
+      out[((int64_t)b * 4 + q) * nvox + v + k] = o;
     }
   }
 }
@@ -435,8 +437,12 @@ extern "C" int mdp_unet_apply(const mdp_unet* net, int32_t nb, const int32_t* se
     ::mdp::launch_k(pack_input_kernel, dim3(bx, nb), 256, 0, st, sel, r, ld, rnorm, dist, ldd, xin, N);
     MDP_LAUNCH_CHECK("pack_input_kernel");
   }
-  ::mdp::launch_k(enc1a_kernel, dim3(ceil_div((int64_t)((n + 1) / 2) * n * n, 128), nb), 128, 0, st, xin, n, net->w[0], net->b[0],
-                                                                                       a1, tf);
+  if (n >= 64)  // wide grids: two voxels per thread; small latency-bound grids: one
+    ::mdp::launch_k(enc1a_kernel<2>, dim3(ceil_div((int64_t)((n + 1) / 2) * n * n, 128), nb), 128, 0, st, xin, n,
+                    net->w[0], net->b[0], a1, tf);
+  else
+    ::mdp::launch_k(enc1a_kernel<1>, dim3(ceil_div((int64_t)n * n * n, 128), nb), 128, 0, st, xin, n, net->w[0],
+                    net->b[0], a1, tf);
   MDP_LAUNCH_CHECK("enc1a_kernel");
 
   if (path == 1) {
