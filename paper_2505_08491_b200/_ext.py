@@ -12,7 +12,8 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libmdp_b200.so"
+LIB_PATH = Path(os.environ.get("MDP_LIB_PATH", "")  # A/B timing of alternative builds only
+                or Path(__file__).resolve().parent / "lib" / "libmdp_b200.so")
 
 _vp = C.c_void_p
 _i32 = C.c_int32

@@ -105,10 +105,11 @@ __device__ double g_zero_page[kZeroPage];
 #define STENCIL_ROWS 2  // output rows per warp
 #endif
 
-struct GatherArgs {  // optional Pi gather folded into the stencil launch (last y-slice)
+struct GatherArgs {  // optional Pi gather folded into the stencil launch
   const double* x3;
   const double* x1;
   double* s_out;
+  int nblk;  // v3 launch: blocks given to the gather
 };
 
 template <bool JAC, bool GATHER>
@@ -565,8 +566,11 @@ __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* 
   }
 }
 
+#ifndef STENCIL3_MINB
+#define STENCIL3_MINB 1  // lifts the compiler's 128-register choice (129^3 x 8: 2.8 -> 3.6 TB/s)
+#endif
 template <int N, int RY, bool JAC>
-__global__ void __launch_bounds__(256) stencil3_kernel(const mdp_problem P, const int32_t* sel,
+__global__ void __launch_bounds__(256, STENCIL3_MINB) stencil3_kernel(const mdp_problem P, const int32_t* sel,
                                                         const double* __restrict__ x, int64_t ldx,
                                                         double* __restrict__ y, int64_t ldy, int zchunk,
                                                         const double* __restrict__ jr, double omega,
@@ -575,10 +579,14 @@ __global__ void __launch_bounds__(256) stencil3_kernel(const mdp_problem P, cons
   MDP_PDL_ENTER();
   constexpr int NR = RY + 2;
   const int n = N > 0 ? N : P.n;
-  const int s = sys_of(sel, blockIdx.z);
-  if (G.s_out && blockIdx.y == gridDim.y - 1) {
-    gather_rows(P, s, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5), G.x3, G.x1,
-                ldx, G.s_out);
+  // grid (x: block slot, y: system): slots [0, gx) run the Pi gather (first in
+  // launch order, alongside the first stencil blocks), then one slot per
+  // (band, z-chunk)
+  const int s = sys_of(sel, blockIdx.y);
+  const int gx = G.s_out ? G.nblk : 0;
+  if ((int)blockIdx.x < gx) {
+    gather_rows(P, s, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gx * (blockDim.x >> 5), G.x3, G.x1, ldx,
+                G.s_out);
     return;
   }
   extern __shared__ __align__(16) unsigned char smem3[];
@@ -589,8 +597,10 @@ __global__ void __launch_bounds__(256) stencil3_kernel(const mdp_problem P, cons
   const int sw = (NR * n + 4 + 1) & ~1;  // stage stride in doubles (16-byte multiple)
   const int tiles_x = (n + 31) / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = blockIdx.x * RY;
-  const int z0 = blockIdx.y * zchunk;
+  const int bands = (n + RY - 1) / RY;
+  const int slot = blockIdx.x - gx;
+  const int j = (slot % bands) * RY;
+  const int z0 = (slot / bands) * zchunk;
   const int z1 = min(n, z0 + zchunk);
   if (j >= n || z0 >= n) return;  // gather-slice width / chunk rounding
   const bool dir = P.bc3d != 0;
@@ -824,7 +834,7 @@ static int launch_stencil2(const mdp_problem* p, int32_t nsel, const int32_t* se
   const bool gat = g != nullptr && p->qmax > 0;
   if (gat) bx = bx > ceil_div(p->qmax, 4) ? bx : ceil_div(p->qmax, 4);
   dim3 grid(bx, zch + (gat ? 1 : 0), nsel);
-  const GatherArgs G = gat ? *g : GatherArgs{nullptr, nullptr, nullptr};
+  const GatherArgs G = gat ? *g : GatherArgs{nullptr, nullptr, nullptr, 0};
   static const int pd = env_int("MDP_STENCIL_PD", 6);  // L2 prefetch distance in planes (0: off)
 #define MDP_ST2(NN, R) launch_stencil2_t<NN, R>(grid, st, p, sel, x, ldx, y, ldy, zchunk, jr, omega, G, pd)
   if (RY == 2) {
@@ -893,11 +903,9 @@ static int launch_stencil3(const mdp_problem* p, int32_t nsel, const int32_t* se
   if (forced > 0) zchunk = forced < n ? forced : n;
   zch = ceil_div(n, zchunk);
   const bool gat = g != nullptr && p->qmax > 0;
-  int bx = bands;
-  const int wpb = tiles_x + 1;
-  if (gat) bx = bx > ceil_div(p->qmax, wpb) ? bx : ceil_div(p->qmax, wpb);
-  dim3 grid(bx, zch + (gat ? 1 : 0), nsel);
-  const GatherArgs G = gat ? *g : GatherArgs{nullptr, nullptr, nullptr};
+  GatherArgs G = gat ? *g : GatherArgs{nullptr, nullptr, nullptr, 0};
+  if (gat) G.nblk = ceil_div(p->qmax, (tiles_x + 1) * 2);  // ~2 quadrature rows per warp
+  dim3 grid(G.nblk + bands * zch, nsel);
 #define MDP_ST3L(NN, R) \
   launch_stencil3_t<NN, R>(grid, threads, smem, st, p, sel, x, ldx, y, ldy, zchunk, jr, omega, G)
   if (RY == 2) {
@@ -951,7 +959,7 @@ static int launch_stencil(const mdp_problem* p, int32_t nsel, const int32_t* sel
   const bool gat = g != nullptr && p->qmax > 0;
   if (gat) bx = bx > ceil_div(p->qmax, 4) ? bx : ceil_div(p->qmax, 4);  // one warp per Pi row in the gather slice
   dim3 grid(bx, zch + (gat ? 1 : 0), nsel);
-  GatherArgs G = gat ? *g : GatherArgs{nullptr, nullptr, nullptr};
+  GatherArgs G = gat ? *g : GatherArgs{nullptr, nullptr, nullptr, 0};
   if (jr) {
     if (gat)
       ::mdp::launch_k(stencil_kernel<true, true>, grid, 128, 0, st, *p, sel, x, ldx, y, ldy, zchunk, jr, omega, G);

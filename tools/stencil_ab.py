@@ -48,11 +48,14 @@ def child(cases):
         t_st = timed(lambda: ops.stencil(X, Y))
         t_c = timed(lambda: A.matvec(X, Y))
         t_cp = timed(lambda: Y.copy_(X))
+        t_g = timed(lambda: ops.gather(X, None, p.s_work))
+        t_s = timed(lambda: ops.scatter(p.s_work, 1.0, Y))
         b_st = 16 * p.n3 * nb
         b_c = sum(16 * (p.n3 + int(n1)) for n1 in p.n1) + 40 * p.Qtot
         out.append({"n": n, "nb": nb, "stencil_us": round(t_st * 1e3, 2), "stencil_GBps": round(b_st / t_st / 1e6, 1),
                     "coupled_us": round(t_c * 1e3, 2), "coupled_GBps": round(b_c / t_c / 1e6, 1),
-                    "copy_GBps": round(2 * X.numel() * 8 / t_cp / 1e6, 1)})
+                    "copy_GBps": round(2 * X.numel() * 8 / t_cp / 1e6, 1), "gather_us": round(t_g * 1e3, 2),
+                    "pull_us": round(t_s * 1e3, 2)})
         del p, A, ops, X, Y
         torch.cuda.empty_cache()
     print("RESULT " + json.dumps(out))
