@@ -111,11 +111,18 @@ class FgmresEngine:
         self.vcur = torch.zeros((nsys, ld), **f)
         self.zcur = torch.zeros((nsys, ld), **f)
         self.tmp = torch.zeros((nsys, ld), **f)
-        # Hessenberg columns [nsys][k+2] followed by one flag per system (graph steps)
-        self.hbuf = torch.zeros(nsys * (restart + 2) + nsys, **f)
-        self.hcol = self.hbuf[:nsys * (restart + 2)].view(nsys, restart + 2)
-        self.pflag = self.hbuf[nsys * (restart + 2):]
+        # Hessenberg columns [nsys][k+2] followed by one flag per system (graph
+        # steps); two parities so a speculative step can run while the host
+        # reads the previous one
+        self._hb = []
+        for _ in range(2):
+            hb = torch.zeros(nsys * (restart + 2) + nsys, **f)
+            self._hb.append((hb, hb[:nsys * (restart + 2)].view(nsys, restart + 2), hb[nsys * (restart + 2):]))
+        self._use_parity(0)
+        self._par = 0
         self._graphs = {}
+        self.speculative = True      # enqueue step j+1 before reading step j (graph path)
+        self.spec_discarded = 0      # speculative steps thrown away (cycle ends / exact redo)
         self.replayed_kernels = 0  # our kernels executed through graph replays
         self.rn = torch.zeros(nsys, **f)
         self.ybuf = torch.zeros((nsys, restart), **f)
@@ -130,11 +137,14 @@ class FgmresEngine:
         # one pinned staging slot + device copy per upload purpose: a slot is
         # rewritten only after a stream synchronisation since its last copy
         self._regions = {}
-        for name in ("all", "start", "arn", "js", "nv", "end", "cnt", "res", "redo", "rjs", "rnv"):
+        for name in ("all", "start", "arn0", "js0", "nv0", "arn1", "js1", "nv1", "end", "cnt", "res", "redo", "rjs",
+                     "rnv"):
             self._regions[name] = (torch.zeros(nsys, dtype=torch.int32, pin_memory=True),
                                    torch.zeros(nsys, dtype=torch.int32, device=device))
 
     # -- small helpers -------------------------------------------------------------
+    def _use_parity(self, par):
+        self.hbuf, self.hcol, self.pflag = self._hb[par]
     def _upload(self, name, values):
         """Small int32 list -> device through its dedicated pinned slot."""
         import torch
@@ -188,17 +198,40 @@ class FgmresEngine:
         _ext.check(self.lib.mdp_copy_slot(m, sel.data_ptr(), self.V.data_ptr(), (k + 1) * self.ld, jd.data_ptr(),
                                           self.ld, self.vcur.data_ptr(), self.ld, self.n, _ext.stream()))
 
-    def _read_h(self, m, with_flags=False):
+    def _read_h(self, m, with_flags=False, then=None):
+        """Hessenberg columns (+ flags) of the current parity to the host.
+
+        ``then()`` is enqueued after the copies and before the wait, which
+        covers only the work up to the copies (a speculative step keeps the
+        device busy meanwhile)."""
         import torch
         kk = self.k + 2
         nf = self.nsys * kk
         self.h_host[:m * kk].copy_(self.hbuf[:m * kk], non_blocking=True)
         if with_flags:
             self.h_host[nf:nf + m].copy_(self.pflag[:m], non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        ev = torch.cuda.Event()
+        ev.record()
+        if then is not None:
+            then()
+        ev.synchronize()
         h = self.h_host[:m * kk].numpy().reshape(m, kk)
         f = self.h_host[nf:nf + m].numpy() if with_flags else None
         return h, f
+
+    def _graph(self, A, Pg, arn, par, js):
+        """(graph, launches) of one Arnoldi step for the active set ``arn`` with
+        the parity-``par`` buffers; uploads this step's j values."""
+        key = (tuple(arn), par)
+        sel = self._upload(f"arn{par}", arn)
+        jd = self._upload(f"js{par}", js)
+        nv = self._upload(f"nv{par}", [j + 1 for j in js])
+        g = self._graphs.get(key)
+        if g is None:
+            self._use_parity(par)
+            g = self._capture(A, Pg, sel, jd, nv, len(arn), list(arn))
+            self._graphs[key] = g
+        return g, sel, jd
 
     def _sync_read(self, dev, host, m):
         import torch
@@ -257,6 +290,8 @@ class FgmresEngine:
             else:
                 starting.append(s)
         arn = []          # systems currently inside a cycle
+        spec = None       # (systems, js, parity) of a speculatively enqueued Arnoldi step
+        stale = False     # vcur advanced by a discarded speculative step
         while True:
             # ---- cycle starts (krylov.py:123-134)
             if starting:
@@ -296,21 +331,43 @@ class FgmresEngine:
             arn.sort()
             # ---- one Arnoldi step for every system inside a cycle (krylov.py:135-167)
             js = [st[s].j for s in arn]
-            sel = self._upload("arn", arn)
-            jd = self._upload("js", js)
-            nv = self._upload("nv", [j + 1 for j in js])
             ma = len(arn)
             if Pg is not None:
-                key = tuple(arn)
-                g = self._graphs.get(key)
-                if g is None:
-                    g = self._capture(A, Pg, sel, jd, nv, ma, arn)
-                    self._graphs[key] = g
-                g[0].replay()
-                self.replayed_kernels += g[1]
-                hb = self._read_h(ma, with_flags=True)
+                if spec is not None and spec[0] == tuple(arn) and spec[1] == js:
+                    par = spec[2]  # this step is already enqueued (speculatively)
+                else:
+                    # the parity not used by the last enqueued step (its uploads are done)
+                    par = self._par = self._par ^ 1
+                    g, sel, jd = self._graph(A, Pg, arn, par, js)
+                    if spec is not None or stale:
+                        # a discarded speculative step advanced vcur: restore V[j]
+                        self._gather_slot(sel, jd, ma)
+                        self.spec_discarded += 1
+                    self._use_parity(par)
+                    g[0].replay()
+                    self.replayed_kernels += g[1]
+                spec, stale = None, False
+                self._use_parity(par)
+                # speculate: enqueue step j+1 for the same systems (a cycle end or
+                # an exact redo below discards it); only with a captured graph
+                nxt = None
+                if self.speculative and all(st[s].j + 1 < k and st[s].iters + 1 < maxit for s in arn) \
+                        and (tuple(arn), par ^ 1) in self._graphs:
+                    def nxt(arn=arn, q=par ^ 1, js1=[j + 1 for j in js]):
+                        nonlocal spec
+                        g1 = self._graph(A, Pg, arn, q, js1)[0]
+                        g1[0].replay()
+                        self.replayed_kernels += g1[1]
+                        self._par = q
+                        spec = (tuple(arn), js1, q)
+                hb = self._read_h(ma, with_flags=True, then=nxt)
+                self._use_parity(par)
                 redo = [s for i, s in enumerate(arn) if hb[1][i] != 0.0]
                 if redo:
+                    if spec is not None:
+                        # the speculative step used the flagged systems' inexact step j:
+                        # discard it (stream order keeps it ahead of the redo below)
+                        spec, stale = None, True
                     # exact host-driven path for systems whose graph step hit a flagged case
                     rsel = self._upload("redo", redo)
                     rj = self._upload("rjs", [st[s].j for s in redo])
@@ -326,6 +383,9 @@ class FgmresEngine:
                 else:
                     hc = hb[0]
             else:
+                sel = self._upload("arn0", arn)
+                jd = self._upload("js0", js)
+                nv = self._upload("nv0", [j + 1 for j in js])
                 self._step(A, P, sel, jd, nv, ma, arn)
                 hc = self._read_h(ma)[0]
             ending = []
