@@ -270,3 +270,74 @@ def test_arnoldi_kernel_orthogonalises(gpu):
     vnext = V[0, k].cpu().numpy()
     assert np.allclose(vnext, wr / np.linalg.norm(wr), atol=1e-12)
     assert np.max(np.abs(Q.T @ vnext)) <= 1e-13
+
+
+def _dirichlet_k00(x3, n, h, kO, sO):
+    """Dirichlet-cube K00: eliminated boundary columns, unit boundary rows."""
+    v = x3.reshape(n, n, n).copy()
+    inner = np.zeros((n, n, n), dtype=bool)
+    inner[1:-1, 1:-1, 1:-1] = True
+    y = _kron_k00(np.where(inner, v, 0.0).ravel(), n, h, kO, sO).reshape(n, n, n)
+    return np.where(inner, y, v).ravel()
+
+
+@pytest.mark.parametrize("n", [17, 33, 65, 129, 193])
+@pytest.mark.parametrize("bc3d", ["neumann", "dirichlet"])
+def test_stencil_configured_sizes_vs_kronecker(gpu, n, bc3d):
+    """The compile-time-n instantiations of the v3 stencil (17/33: 2-row bands,
+    65/129/193: 4-row bands), two systems in one launch, against the Kronecker
+    restatement of K00 (assembly.py:83-125) with the Dirichlet-cube elimination."""
+    import torch
+    from paper_2505_08491_b200 import assembly as A, geometry as G
+    from paper_2505_08491_b200.operators import CouplingOps
+    grid = G.StructuredGrid(n)
+    systems = [A.assemble_coupled_system(grid, G.random_tree(2, 5 + i, 1e-3), A.PhysicalParams(epsilon=1e-3),
+                                         elems_per_edge=2, bc3d=bc3d) for i in range(2)]
+    pb = A.DeviceProblem(systems)
+    rng = np.random.default_rng(n)
+    xs = [rng.standard_normal(pb.n3) for _ in range(2)]
+    X, Y = pb.zeros(), pb.zeros()
+    for i, x in enumerate(xs):
+        X[i, :pb.n3] = torch.as_tensor(x, device="cuda")
+    CouplingOps(pb).stencil(X, Y)
+    p = systems[0].params
+    f = _dirichlet_k00 if bc3d == "dirichlet" else _kron_k00
+    for i, x in enumerate(xs):
+        want = f(x, n, 1.0 / (n - 1), p.k_omega, p.sigma_omega)
+        assert rel(Y[i, :pb.n3].cpu().numpy(), want) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [129])
+def test_jacobi_sweep_large_vs_device_spmv(gpu, n):
+    """Fused Jacobi epilogue of the n=129 instantiation against x + w (r - C x) / diag(C)
+    formed from the device SpMV (which the reference-vector tests pin)."""
+    import torch
+    from paper_2505_08491_b200 import configs
+    from paper_2505_08491_b200.assembly import DeviceProblem
+    from paper_2505_08491_b200.operators import ReducedOperator
+    pb = DeviceProblem(configs.cfg5_systems(n, 2))
+    op = ReducedOperator(pb)
+    X, Rr, Xo, T, CX = (pb.zeros() for _ in range(5))
+    X[:, :pb.n3].normal_()
+    Rr[:, :pb.n3].normal_()
+    op.jacobi(Rr, X, Xo, 2.0 / 3.0, T)
+    op.matvec(X, CX)
+    d = pb._t["diag_c"].view(pb.nsys, pb.ld)
+    want = X + (2.0 / 3.0) * (Rr - CX) / d
+    for i in range(pb.nsys):
+        assert rel(Xo[i, :pb.n3].cpu().numpy(), want[i, :pb.n3].cpu().numpy()) <= 1e-12
+
+
+def test_coupled_spmv_129_batched_equals_serial_bitwise(gpu):
+    import torch
+    from paper_2505_08491_b200 import configs
+    from paper_2505_08491_b200.assembly import DeviceProblem
+    from paper_2505_08491_b200.operators import CoupledOperator
+    pb = DeviceProblem(configs.cfg5_systems(129, 3))
+    X = pb.zeros().normal_()
+    Y = pb.zeros()
+    CoupledOperator(pb).matvec(X, Y)
+    for i in range(pb.nsys):
+        Yi = pb.zeros()
+        CoupledOperator(pb).matvec(X, Yi, torch.tensor([i], dtype=torch.int32, device="cuda"))
+        assert torch.equal(Yi[i], Y[i])
