@@ -139,10 +139,14 @@ typedef struct mdp_ilu {
   const int32_t* nlev_f;     /* [nsys]                                     */
   const int32_t* nlev_b;     /* [nsys]                                     */
   int32_t max_rows, max_nnz; /* per-system maxima (shared-memory staging)  */
+  const int32_t* perm;       /* optional [Rtot] symmetric permutation: the factor is
+                                of P A P^T, z = P^T (LU)^-1 P r (NULL: identity) */
 } mdp_ilu;
 
 /* z1 = (LU)^-1 r1, bitwise equal to krylov.ilu0_apply (krylov.py:219-233,
- * 270-276).  r/z point at the 1D parts; stride ld. */
+ * 270-276).  r/z point at the 1D parts; stride ld.  With perm set (a
+ * fill-free leaf-first order of the tree-structured A11) the same sweeps are
+ * the exact solve of one_d="direct" (harness.py:356-358). */
 int mdp_ilu0_apply(const mdp_ilu* f, int32_t nsel, const int32_t* sel,
                    const double* r, double* z, int64_t ld, void* stream);
 

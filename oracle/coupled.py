@@ -2,7 +2,8 @@
 
 TEST INFRASTRUCTURE ONLY (see ``oracle/__init__.py``).
 Restates ``harness.solve_coupled`` (harness.py:324-406) for the one_d='ilu0'
-strategy with a 3D inner preconditioner of type none / ilu0 / neural.
+and 'direct' strategies with a 3D inner preconditioner of type none / ilu0 /
+neural.
 """
 
 from __future__ import annotations
@@ -18,13 +19,14 @@ from .unet import apply_neural
 
 @dataclass
 class CoupledStrategy:
-    """harness.py:324-339 (one_d fixed to 'ilu0')."""
+    """harness.py:324-339 (one_d 'ilu0' or 'direct')."""
 
     tol: float = 1e-15
     maxit: int = 2000
     restart: int = 20
     inner_iterations: int = 3
     three_d: dict | None = None     # {"type": "none"|"ilu0"|"neural", "params":..., "smoothing":(m, w)}
+    one_d: str = "ilu0"             # "ilu0" | "direct" (splu of A11, harness.py:356-358)
 
 
 def mesh_distance_field(s: P.CoupledSystem) -> np.ndarray:
@@ -55,7 +57,15 @@ def solve_coupled(s: P.CoupledSystem, st: CoupledStrategy, dvals=None):
     w = s.params.coupling_weight
     A11 = P.one_d_operator(s)
     C = P.reduced_operator(s)
-    fact = ilu0(A11)
+    if st.one_d == "direct":
+        import scipy.sparse.linalg as spla
+        lu11 = spla.splu(A11.tocsc())
+        apply_1d = lu11.solve
+    elif st.one_d == "ilu0":
+        fact = ilu0(A11)
+        apply_1d = lambda r: ilu0_apply(fact, r)  # noqa: E731
+    else:
+        raise ValueError(f"oracle one_d strategy {st.one_d!r} not restated")
     spec = st.three_d or {"type": "none"}
     if spec.get("type") == "neural" and dvals is None:
         dvals = mesh_distance_field(s)
@@ -63,7 +73,7 @@ def solve_coupled(s: P.CoupledSystem, st: CoupledStrategy, dvals=None):
     m = st.inner_iterations
 
     def block_precond(r):
-        z1 = ilu0_apply(fact, r[n3:])
+        z1 = apply_1d(r[n3:])
         z0, _ = fgmres(C, inner, r[:n3] - w * (s.M01 @ z1), restart=m, tol=1e-300, maxit=m)
         return np.concatenate([z0, z1])
 

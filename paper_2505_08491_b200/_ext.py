@@ -36,7 +36,7 @@ class MdpIlu(C.Structure):
     _fields_ = [("nsys", _i32), ("lev_stride", _i32), ("row_start", _vp), ("ptr", _vp),
                 ("col", _vp), ("val", _vp), ("diag", _vp), ("lev_f", _vp), ("perm_f", _vp),
                 ("lev_b", _vp), ("perm_b", _vp), ("nlev_f", _vp), ("nlev_b", _vp),
-                ("max_rows", _i32), ("max_nnz", _i32)]
+                ("max_rows", _i32), ("max_nnz", _i32), ("perm", _vp)]
 
 
 class MdpUnet(C.Structure):

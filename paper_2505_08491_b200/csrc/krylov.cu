@@ -427,7 +427,6 @@ __global__ void __launch_bounds__(256) ilu0_apply_kernel(const mdp_ilu F, const 
       dsh[t] = F.diag[rs + t] - p0;
       pfs[t] = pf[t];
       pbs[t] = pb[t];
-      xsh[t] = rp[t];  // the forward sweep reads r[row] before writing xsh[row]
     }
     for (int t = threadIdx.x; t <= nlf; t += blockDim.x) lfs[t] = levf[t];
     for (int t = threadIdx.x; t <= nlb; t += blockDim.x) lbs[t] = levb[t];
@@ -438,13 +437,16 @@ __global__ void __launch_bounds__(256) ilu0_apply_kernel(const mdp_ilu F, const 
     pf = pfs;
     pb = pbs;
   }
+  // x = P r (the forward sweep reads x[row] before writing it)
+  const int32_t* gp = F.perm ? F.perm + rs : nullptr;
+  for (int t = threadIdx.x; t < nrow; t += blockDim.x) xsh[t] = rp[gp ? gp[t] : t];
   __syncthreads();
   for (int L = 0; L < nlf; ++L) {
     for (int t = levf[L] + threadIdx.x; t < levf[L + 1]; t += blockDim.x) {
       const int row = pf[t];
       const int a = staged ? psh[row] : F.ptr[rs + row] - p0;
       const int d = staged ? dsh[row] : F.diag[rs + row] - p0;
-      double acc = staged ? xsh[row] : rp[row];
+      double acc = xsh[row];
       for (int p = a; p < d; ++p) acc = __dsub_rn(acc, __dmul_rn(val[p], xsh[col[p]]));
       xsh[row] = acc;
     }
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(256) ilu0_apply_kernel(const mdp_ilu F, const 
     __syncthreads();
   }
   double* zp = z + s * ld;
-  for (int t = threadIdx.x; t < nrow; t += blockDim.x) zp[t] = xsh[t];
+  for (int t = threadIdx.x; t < nrow; t += blockDim.x) zp[gp ? gp[t] : t] = xsh[t];
 }
 
 // ---- device-side Hessenberg work for the fixed-step inner FGMRES ----------

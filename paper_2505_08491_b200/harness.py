@@ -21,7 +21,7 @@ import numpy as np
 from . import _ext
 from .assembly import CoupledSystem, DeviceProblem, full_rhs, one_d_operator
 from .geometry import DistanceField, distance_field_device
-from .krylov import DeviceIlu, FgmresEngine, FixedStepFgmres, IluPreconditioner, SolveReport, ilu0
+from .krylov import DeviceIlu, FgmresEngine, FixedStepFgmres, IluPreconditioner, SolveReport, direct_1d, ilu0
 from .neural import PATH_TCGEN05, UNetParams, device_net, load_checkpoint
 from .operators import CoupledOperator, CouplingOps, ReducedOperator
 from .training import BatchedNeural, NeuralPreconditioner
@@ -29,7 +29,9 @@ from .training import BatchedNeural, NeuralPreconditioner
 
 @dataclass
 class CoupledStrategy:
-    """harness.py:324-339.  ``one_d`` must be 'ilu0' (the reference default)."""
+    """harness.py:324-339.  ``one_d``: 'ilu0' (the reference default) or 'direct'
+    (exact 1D solve, harness.py:356-358); 'schur' (a dense Schur complement
+    built from N1 sparse-direct 3D solves) is not on the device path."""
 
     tol: float = 1e-15
     maxit: int = 2000
@@ -70,8 +72,8 @@ class CoupledSolver:
 
     def __init__(self, systems, strategy: CoupledStrategy, path: int = PATH_TCGEN05, graphs: bool = True):
         import torch
-        if strategy.one_d != "ilu0":
-            raise ValueError("the device path implements the one_d='ilu0' strategy")
+        if strategy.one_d not in ("ilu0", "direct"):
+            raise ValueError(f"one_d={strategy.one_d!r}: the device path implements 'ilu0' and 'direct'")
         self.systems = list(systems)
         self.st = strategy
         self.prob = DeviceProblem(self.systems)
@@ -79,7 +81,8 @@ class CoupledSolver:
         self.A = CoupledOperator(p)
         self.C = ReducedOperator(p)
         self.cpl = CouplingOps(p)
-        self.ilu = DeviceIlu([ilu0(one_d_operator(s)) for s in self.systems])
+        fac = direct_1d if strategy.one_d == "direct" else ilu0
+        self.ilu = DeviceIlu([fac(one_d_operator(s)) for s in self.systems])
         self.lib = _ext.lib()
         spec = strategy.three_d or {"type": "none"}
         kind = spec.get("type", "none")

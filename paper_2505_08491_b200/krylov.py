@@ -660,6 +660,59 @@ def ilu0(A) -> IluFactorization:
     return IluFactorization(A)
 
 
+def tree_elimination_order(A) -> np.ndarray:
+    """Leaf-first (perfect) elimination order of a matrix whose graph is a forest.
+
+    The 1D block A11 = K11 + w M11 of a tree-shaped vessel graph (eliminated
+    Dirichlet rows decoupled) is tree-structured, so LU in this order creates
+    no fill: ILU(0) of P A P^T is then the exact factorisation.  Raises
+    ValueError when the graph has a cycle.
+    """
+    A = sp.csr_matrix(A)
+    n = A.shape[0]
+    G = (abs(A) + abs(A.T)).tocsr()
+    G.setdiag(0)
+    G.eliminate_zeros()
+    deg = np.diff(G.indptr).astype(np.int64)
+    queued = deg <= 1
+    queue = list(np.nonzero(queued)[0])
+    done = np.zeros(n, dtype=bool)
+    order = []
+    head = 0
+    while head < len(queue):
+        v = int(queue[head])
+        head += 1
+        done[v] = True
+        order.append(v)
+        for u in G.indices[G.indptr[v]:G.indptr[v + 1]]:
+            if not done[u]:
+                deg[u] -= 1
+                if deg[u] <= 1 and not queued[u]:
+                    queued[u] = True
+                    queue.append(u)
+    if len(order) != n:
+        raise ValueError("one_d='direct' needs a tree-structured 1D block (the graph has a cycle)")
+    return np.asarray(order, dtype=np.int32)
+
+
+class DirectFactorization(IluFactorization):
+    """Exact LU of a tree-structured 1D block: ILU(0) of P A P^T in a leaf-first
+    order (no fill, so no dropped terms).  Device sweeps apply
+    z = P^T (LU)^-1 P r; replaces splu(A11).solve (harness.py:356-358)."""
+
+    def __init__(self, A):
+        A = sp.csr_matrix(A)
+        perm = tree_elimination_order(A)
+        B = A[perm][:, perm].tocsr()
+        B.sort_indices()
+        super().__init__(B)
+        self.perm = perm
+
+
+def direct_1d(A) -> DirectFactorization:
+    return DirectFactorization(A)
+
+
 class DeviceIlu:
     """Batched device sweeps of per-system ILU(0) factors (``mdp_ilu``)."""
 
@@ -682,11 +735,15 @@ class DeviceIlu:
             lev_b[i, :f.nlev_b + 1] = f.lev_b[:f.nlev_b + 1]
         if max(rows) > 25000:
             raise ValueError("1D block too large for the single-CTA ILU sweep (shared memory)")
+        perms = [getattr(f, "perm", None) for f in factors]
         T = lambda a, dt=torch.int32: torch.as_tensor(np.ascontiguousarray(a).ravel(), dtype=dt, device=device)  # noqa: E731
         self._t = dict(row_start=T(row_start), ptr=T(ptr), col=T(col), val=T(val, torch.float64), diag=T(diag),
                        lev_f=T(lev_f), perm_f=T(np.concatenate([f.perm_f for f in factors])),
                        lev_b=T(lev_b), perm_b=T(np.concatenate([f.perm_b for f in factors])),
                        nlev_f=T([f.nlev_f for f in factors]), nlev_b=T([f.nlev_b for f in factors]))
+        if any(pm is not None for pm in perms):
+            self._t["perm"] = T(np.concatenate([np.arange(r, dtype=np.int32) if pm is None else pm
+                                                for pm, r in zip(perms, rows)]))
         d = _ext.MdpIlu()
         d.nsys, d.lev_stride = nsys, stride
         d.max_rows, d.max_nnz = max(rows), max(nnz)
@@ -702,7 +759,8 @@ class DeviceIlu:
 
 
 def ilu0_apply(fact: IluFactorization, r):
-    """Host-vector drop-in for krylov.ilu0_apply (krylov.py:270-276), run on the device."""
+    """Host-vector drop-in for krylov.ilu0_apply (krylov.py:270-276), run on the device
+    (a DirectFactorization gives the exact solve of one_d='direct')."""
     import torch
     r = np.asarray(r, dtype=float)
     if r.shape != (fact.shape[0],):

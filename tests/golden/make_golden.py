@@ -329,8 +329,33 @@ def gen_cfg1_solve():
         assembly.refine_graph = _ORIG_REFINE
 
 
+def gen_direct():
+    # one_d="direct" (harness.py:356-358: splu of A11) on the reference n=9 family graph:
+    # the exact 1D solve of seeded vectors and two coupled solves with it
+    import scipy.sparse.linalg as spla
+    grid = geometry.StructuredGrid(9)
+    g = geometry.generate_graph(geometry.GraphFamilySpec(n_branches=5), 3)
+    s = assembly.assemble_coupled_system(grid, g, assembly.PhysicalParams())
+    A11 = assembly.one_d_operator(s)
+    rng = np.random.default_rng(11)
+    r1 = rng.standard_normal((3, s.n1))
+    lu = spla.splu(A11.tocsc())
+    out = {"r1": r1, "z1": np.array([lu.solve(r) for r in r1])}
+    for label, spec in (("none", {"type": "none"}), ("ilu0", {"type": "ilu0"})):
+        st = harness.CoupledStrategy(tol=1e-6, maxit=120, restart=30, inner_iterations=3,
+                                     one_d="direct", three_d=spec)
+        u3, u1, rep = harness.solve_coupled(s, st)
+        out[f"solve_{label}_iters"] = np.array(rep.iterations)
+        out[f"solve_{label}_conv"] = np.array(rep.converged)
+        out[f"solve_{label}_hist"] = np.array(rep.residual_history)
+        out[f"solve_{label}_u3"] = u3
+        out[f"solve_{label}_u1"] = u1
+        print("direct", label, rep.iterations, rep.converged, rep.rel_residual)
+    dump("direct_n9", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["assembly", "fgmres", "unet", "apply", "cfg1"]
+    which = sys.argv[1:] or ["assembly", "fgmres", "unet", "apply", "cfg1", "direct"]
     if "assembly" in which:
         gen_assembly()
     if "fgmres" in which:
@@ -341,3 +366,5 @@ if __name__ == "__main__":
         gen_apply_and_solve()
     if "cfg1" in which:
         gen_cfg1_solve()
+    if "direct" in which:
+        gen_direct()

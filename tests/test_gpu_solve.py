@@ -179,3 +179,54 @@ def test_fgmres_dropin_with_device_operator(gpu, tmp_path):
         krylov.fgmres(C, 3.0, b)
     with pytest.raises(ValueError):
         krylov.fgmres(C, None, b, restart=0)
+
+
+def test_direct_1d_apply_vs_reference(gpu):
+    """one_d='direct': device sweeps of the leaf-first exact factor vs splu(A11).solve (harness.py:356-358)."""
+    from paper_2505_08491_b200 import assembly as A
+    from paper_2505_08491_b200.krylov import direct_1d, ilu0_apply
+    g = golden("direct_n9")
+    f = direct_1d(A.one_d_operator(_n9()))
+    for r, z in zip(g["r1"], g["z1"]):
+        assert np.linalg.norm(ilu0_apply(f, r) - z) <= 1e-12 * np.linalg.norm(z)
+
+
+def test_direct_1d_batched_random_trees(gpu):
+    """Batched exact 1D solves on BASELINE random trees (junction vertices: ILU(0) would drop fill)."""
+    import scipy.sparse.linalg as spla
+    import torch
+    from paper_2505_08491_b200 import assembly as A, geometry as G
+    from paper_2505_08491_b200.krylov import DeviceIlu, direct_1d
+    grid = G.StructuredGrid(33)
+    systems = [A.assemble_coupled_system(grid, G.random_tree(8 + 8 * i, 30 + i, 0.015),
+                                         A.PhysicalParams(epsilon=0.015, beta=1.0), elems_per_edge=16,
+                                         bc3d="dirichlet", f1d=1.0) for i in range(3)]
+    mats = [A.one_d_operator(s) for s in systems]
+    dev = DeviceIlu([direct_1d(M) for M in mats])
+    ld = max(M.shape[0] for M in mats) + 7
+    rng = np.random.default_rng(3)
+    R = torch.zeros((3, ld), dtype=torch.float64, device="cuda")
+    rs = [rng.standard_normal(M.shape[0]) for M in mats]
+    for i, r in enumerate(rs):
+        R[i, :len(r)] = torch.as_tensor(r, device="cuda")
+    Z = torch.zeros_like(R)
+    dev.apply(R, Z, ld, nsys=3)
+    for i, (M, r) in enumerate(zip(mats, rs)):
+        want = spla.spsolve(M.tocsc(), r)
+        assert np.linalg.norm(Z[i, :len(r)].cpu().numpy() - want) <= 1e-12 * np.linalg.norm(want)
+
+
+@pytest.mark.parametrize("label", ["none"])  # the 3D ilu0 inner preconditioner is not on the device path
+def test_solve_coupled_direct_1d_vs_reference(gpu, label):
+    from paper_2505_08491_b200 import harness
+    g = golden("direct_n9")
+    s = _n9()
+    st = harness.CoupledStrategy(tol=1e-6, maxit=120, restart=30, inner_iterations=3, one_d="direct",
+                                 three_d={"type": label})
+    u3, u1, rep = harness.solve_coupled(s, st)
+    want = int(g[f"solve_{label}_iters"])
+    assert rep.converged == bool(g[f"solve_{label}_conv"])
+    assert abs(rep.iterations - want) <= (0 if label == "none" else 1)
+    assert rep.rel_residual <= 1e-6
+    assert np.linalg.norm(u3 - g[f"solve_{label}_u3"]) <= 1e-5 * np.linalg.norm(g[f"solve_{label}_u3"])
+    assert np.linalg.norm(u1 - g[f"solve_{label}_u1"]) <= 1e-5 * np.linalg.norm(g[f"solve_{label}_u1"])

@@ -112,3 +112,23 @@ def test_refine_fixed_m_order():
     assert len(m.elements) == 80
     om = OP.refine_graph(OP.random_tree(5, 11, 0.01), 0.1, 16)
     assert np.array_equal(m.coords, om.coords) and np.array_equal(m.elements, om.elements)
+
+
+def test_tree_elimination_order_is_fill_free():
+    """Leaf-first order of a tree-structured A11: the ILU(0) factor of P A P^T is exact (L U == P A P^T)."""
+    import scipy.sparse as sp
+    from paper_2505_08491_b200 import assembly as A, geometry as G
+    from paper_2505_08491_b200.krylov import direct_1d, tree_elimination_order
+    s = A.assemble_coupled_system(G.StructuredGrid(17), G.random_tree(12, 7, 0.02),
+                                  A.PhysicalParams(epsilon=0.02, beta=1.0), elems_per_edge=8)
+    M = A.one_d_operator(s)
+    f = direct_1d(M)
+    F = sp.csr_matrix((f.data, f.indices, f.indptr), shape=f.shape)
+    L = sp.tril(F, -1) + sp.identity(f.shape[0])
+    U = sp.triu(F)
+    B = M[f.perm][:, f.perm]
+    assert abs(L @ U - B).max() <= 1e-12 * abs(B).max()
+    # a cycle has no fill-free order
+    C = sp.csr_matrix(np.array([[2.0, -1, -1], [-1, 2, -1], [-1, -1, 2]]))
+    with pytest.raises(ValueError):
+        tree_elimination_order(C)

@@ -206,3 +206,22 @@ def test_coupled_solve_n9(label, tmp_path):
     assert rep.converged == bool(g[f"solve_{label}_conv"])
     assert np.allclose(rep.residual_history, g[f"solve_{label}_hist"], rtol=1e-6, atol=1e-12)
     assert np.allclose(u3, g[f"solve_{label}_u3"], rtol=1e-8, atol=1e-10)
+
+
+@pytest.mark.parametrize("label", ["none", "ilu0"])
+def test_coupled_solve_n9_direct_1d(label):
+    """one_d='direct' (harness.py:356-358) pinned to the reference's solves."""
+    g = golden("direct_n9")
+    s = _n9_system()
+    A11 = P.one_d_operator(s)
+    import scipy.sparse.linalg as spla
+    z1 = np.array([spla.spsolve(A11.tocsc(), r) for r in g["r1"]])
+    assert np.max(np.abs(z1 - g["z1"])) <= 1e-12 * np.abs(g["z1"]).max()
+    st = oracle.CoupledStrategy(tol=1e-6, maxit=120, restart=30, inner_iterations=3, three_d={"type": label},
+                                one_d="direct")
+    u3, u1, rep = oracle.solve_coupled(s, st)
+    assert rep.iterations == int(g[f"solve_{label}_iters"])
+    assert rep.converged == bool(g[f"solve_{label}_conv"])
+    assert np.allclose(rep.residual_history, g[f"solve_{label}_hist"], rtol=1e-6, atol=1e-12)
+    assert np.allclose(u3, g[f"solve_{label}_u3"], rtol=1e-8, atol=1e-10)
+    assert np.allclose(u1, g[f"solve_{label}_u1"], rtol=1e-8, atol=1e-10)
