@@ -182,3 +182,67 @@ def distance_field_device(vertices: np.ndarray, edges: np.ndarray, grid: Structu
 def distance_field(graph: Graph1D, grid: StructuredGrid) -> DistanceField:
     """Drop-in for geometry.distance_field (values on the host)."""
     return DistanceField(grid, distance_field_device(graph.vertices, graph.edges, grid).cpu().numpy())
+
+
+# ---------------------------------------------------------------------------
+# file formats (geometry.py:306-363): graph JSON and MDF1 grid vectors
+
+_FIELD_MAGIC = b"MDF1"
+
+
+def save_graph(graph: Graph1D, path) -> None:
+    """Graph as JSON: vertices, edges, radius, dirichlet set (geometry.py:306-316)."""
+    import json
+    doc = {
+        "vertices": [[float(x) for x in v] for v in graph.vertices],
+        "edges": [[int(a), int(b)] for a, b in graph.edges],
+        "radius": float(graph.radius),
+        "dirichlet": [int(i) for i in graph.dirichlet_vertices],
+    }
+    with open(path, "w") as fh:
+        json.dump(doc, fh)
+
+
+def load_graph(path) -> Graph1D:
+    """geometry.py:319-324."""
+    import json
+    with open(path) as fh:
+        doc = json.load(fh)
+    return Graph1D(np.array(doc["vertices"], dtype=float), np.array(doc["edges"], dtype=np.int64),
+                   float(doc["radius"]), tuple(doc["dirichlet"]))
+
+
+def write_grid_vector(path, n: int, values) -> None:
+    """MDF1: magic, u32 n, n**3 little-endian f64 (geometry.py:330-338)."""
+    import struct
+    values = np.asarray(values, dtype="<f8").ravel()
+    if values.size != n ** 3:
+        raise ValueError(f"expected {n ** 3} values for n={n}, got {values.size}")
+    with open(path, "wb") as fh:
+        fh.write(_FIELD_MAGIC)
+        fh.write(struct.pack("<I", n))
+        fh.write(values.tobytes())
+
+
+def read_grid_vector(path) -> tuple:
+    """(n, values) of an MDF1 file; ValueError on a bad magic or truncation (geometry.py:341-353)."""
+    import struct
+    with open(path, "rb") as fh:
+        magic = fh.read(4)
+        if magic != _FIELD_MAGIC:
+            raise ValueError(f"bad magic {magic!r}, expected {_FIELD_MAGIC!r}")
+        (n,) = struct.unpack("<I", fh.read(4))
+        data = fh.read()
+    values = np.frombuffer(data, dtype="<f8")
+    if values.size != n ** 3:
+        raise ValueError("truncated grid-vector file")
+    return int(n), values.astype(float)
+
+
+def save_distance_field(dfield: DistanceField, path) -> None:
+    write_grid_vector(path, dfield.grid.n, dfield.values)
+
+
+def load_distance_field(path) -> DistanceField:
+    n, values = read_grid_vector(path)
+    return DistanceField(StructuredGrid(n), values)

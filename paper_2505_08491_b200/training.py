@@ -170,3 +170,49 @@ class NeuralPreconditioner(Preconditioner):
 
     def apply(self, r):
         return apply_neural(self.params, r, self.dfield, self.smoothing, self.C, self.zero_distance)
+
+
+# ---------------------------------------------------------------------------
+# MDS1 sample files of the dataset directory format (training.py:361-393):
+# magic, u32 count, then per sample u32 tag code + n_h little-endian f64
+
+_SAMPLES_MAGIC = b"MDS1"
+SAMPLE_TAGS = {"physics": 0, "krylov": 1, "random": 2}
+_TAG_NAMES = {v: k for k, v in SAMPLE_TAGS.items()}
+
+
+def write_samples(path, vectors, tags) -> None:
+    """Write (vector, tag) samples; tags in SAMPLE_TAGS."""
+    import struct
+    if len(vectors) != len(tags):
+        raise ValueError("one tag per sample vector")
+    with open(path, "wb") as fh:
+        fh.write(_SAMPLES_MAGIC)
+        fh.write(struct.pack("<I", len(vectors)))
+        for v, t in zip(vectors, tags):
+            fh.write(struct.pack("<I", SAMPLE_TAGS[t]))
+            fh.write(np.asarray(v, dtype="<f8").tobytes())
+
+
+def read_samples(path) -> tuple:
+    """(vectors [count][n_h], tags) of an MDS1 file; ValueError on a bad magic or truncation."""
+    import struct
+    with open(path, "rb") as fh:
+        raw = fh.read()
+    if raw[:4] != _SAMPLES_MAGIC:
+        raise ValueError(f"bad samples magic {raw[:4]!r}")
+    (count,) = struct.unpack_from("<I", raw, 4)
+    if count == 0:
+        return np.zeros((0, 0)), []
+    body = len(raw) - 8
+    if body % count:
+        raise ValueError("truncated samples file")
+    n_h = (body // count - 4) // 8
+    vecs, tags, off = [], [], 8
+    for _ in range(count):
+        (code,) = struct.unpack_from("<I", raw, off)
+        off += 4
+        vecs.append(np.frombuffer(raw, dtype="<f8", count=n_h, offset=off).astype(float))
+        off += 8 * n_h
+        tags.append(_TAG_NAMES[code])
+    return np.array(vecs), tags

@@ -354,8 +354,29 @@ def gen_direct():
     dump("direct_n9", **out)
 
 
+def gen_formats():
+    # interchange files written by the reference (geometry.py:306-363, training.py:361-393)
+    grid = geometry.StructuredGrid(9)
+    g = geometry.generate_graph(geometry.GraphFamilySpec(n_branches=5), 3)
+    d = geometry.distance_field(g, grid)
+    rng = np.random.default_rng(21)
+    vecs = rng.standard_normal((3, grid.num_nodes))
+    vecs /= np.linalg.norm(vecs, axis=1, keepdims=True)  # samples live on the unit sphere
+    tags = ["physics", "krylov", "random"]
+    with tempfile.TemporaryDirectory() as td:
+        td = Path(td)
+        geometry.save_graph(g, td / "g.json")
+        geometry.save_distance_field(d, td / "d.bin")
+        training._write_samples(td / "s.bin", [training.TrainingSample(v, t, 0) for v, t in zip(vecs, tags)])
+        out = {name: np.frombuffer((td / name).read_bytes(), dtype=np.uint8).copy()
+               for name in ("g.json", "d.bin", "s.bin")}
+    dump("formats_n9", graph_json=out["g.json"], mdf1=out["d.bin"], mds1=out["s.bin"], vecs=vecs,
+         tags=np.array(tags), dvalues=d.values, vertices=g.vertices, edges=g.edges,
+         radius=np.array(g.radius), dirichlet=np.array(g.dirichlet_vertices))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["assembly", "fgmres", "unet", "apply", "cfg1", "direct"]
+    which = sys.argv[1:] or ["assembly", "fgmres", "unet", "apply", "cfg1", "direct", "formats"]
     if "assembly" in which:
         gen_assembly()
     if "fgmres" in which:
@@ -368,3 +389,5 @@ if __name__ == "__main__":
         gen_cfg1_solve()
     if "direct" in which:
         gen_direct()
+    if "formats" in which:
+        gen_formats()
