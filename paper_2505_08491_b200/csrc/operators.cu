@@ -76,12 +76,6 @@ __device__ __forceinline__ void gather_rows(const mdp_problem& P, int s, int w0,
 }
 
 __device__ double g_zero_row[32];  // zero page: out-of-domain rows read from here
-// v2 stencil zero page: (RY+2) rows of pitch n plus a warp of columns
-constexpr int kZeroPage = 8192;
-// optional per-step clock trace of block (0,0,0) (tools/stencil_trace.py; off unless enabled)
-__device__ int g_trace_on = 0;
-__device__ long long g_trace[8][512];
-__device__ double g_zero_page[kZeroPage];
 
 // Warp-per-row-pair stencil: lane l owns column i = i0 - 1 + l (30 output
 // columns per warp, lanes 0 and 31 are the x halo), the warp owns rows j,
@@ -234,24 +228,14 @@ __global__ void __launch_bounds__(128) stencil_kernel(const mdp_problem P, const
 }
 
 // ---------------------------------------------------------------------------
-// Stencil v2: fewer instructions per output (the v1 kernel above is
-// issue-bound at ~3.4 instructions per output).  Same warp geometry (lane =
-// x column, 30 outputs per warp, lanes 0/31 the x halo) but
-//  * RY output rows per warp (RY+2 rows loaded per plane, y-neighbours are
-//    registers), the grid size N a template parameter when it is one of the
-//    configured sizes (row offsets become load immediates; N = 0: runtime n);
-//  * the three 1D factors folded into 8 per-lane coefficients: with
-//    S = lr_{j-1} + lr_{j+1}, T = v_{j-1} + v_{j+1} (lr = x_{i-1} + x_{i+1})
-//      U = mo P + ko R = b1 S + b2 T + rho (b3 lr_j + b4 v_j)
-//      C = md P + kd R = c1 S + c2 T + rho (c3 lr_j + c4 v_j)
-//      y_k = U_{k-1} + U_{k+1} + sigma_k C_k
-//    (P, R as in v1; every 1D end-row diagonal is half the interior one, so
-//    Neumann end rows / end planes only scale the centre terms by 0.5:
-//    rho per row, sigma per plane);
-//  * the plane loop unrolled by 6 so the load ring (3 planes) and the U / C
-//    rings are register renaming, no moves; warp-uniform interior / edge
-//    bodies (edge = a row group touching the domain boundary).
-// Determinism: one fixed expression per node (batched == serial bitwise).
+// Folded Kronecker coefficients of the v3 stencil below.  With
+// S = lr_{j-1} + lr_{j+1}, T = v_{j-1} + v_{j+1} (lr = x_{i-1} + x_{i+1}):
+//   U = mo P + ko R = b1 S + b2 T + rho (b3 lr_j + b4 v_j)
+//   C = md P + kd R = c1 S + c2 T + rho (c3 lr_j + c4 v_j)
+//   y_k = U_{k-1} + U_{k+1} + sigma_k C_k
+// (P, R as in v1; every 1D end-row diagonal is half the interior one, so
+// Neumann end rows / end planes only scale the centre terms by 0.5: rho per
+// row, sigma per plane).  One fixed expression per node (batched == serial).
 struct StencilCoef {
   double b1, b2, b3, b4, c1, c2, c3, c4;
 };
@@ -277,169 +261,6 @@ __device__ __forceinline__ StencilCoef stencil_coef(const Line1D& c, double kO, 
   k.c3 = cc * ko + cd * mo;
   k.c4 = cc * kdx + cd * mdx;
   return k;
-}
-
-#ifndef STENCIL2_RY
-#define STENCIL2_RY 4
-#endif
-
-template <int N, int RY, bool JAC, bool DIR, bool EDGE>
-__device__ __forceinline__ void stencil2_body(const mdp_problem& P, const double* __restrict__ xp,
-                                              double* __restrict__ yp, const double* __restrict__ jrp,
-                                              const double* __restrict__ dgp, double omega, int n, int i, int j,
-                                              int z0, int z1, const StencilCoef& K, int pd) {
-  constexpr int NR = RY + 2;
-  const int lane = threadIdx.x & 31;
-  const int64_t nn = (int64_t)n * n;
-  const bool colok = i >= 0 && i < n && !(DIR && (i == 0 || i == n - 1));
-  const bool out_lane = lane >= 1 && lane <= 30 && i < n;
-  // rows: load validity and Neumann end-row scaling (edge bodies only)
-  bool rowok[NR];
-  double rho[RY];
-  bool rbnd[RY];
-#pragma unroll
-  for (int a = 0; a < NR; ++a) {
-    const int jj = j - 1 + a;
-    rowok[a] = !EDGE || (jj >= 0 && jj < n && !(DIR && (jj == 0 || jj == n - 1)));
-  }
-#pragma unroll
-  for (int r = 0; r < RY; ++r) {
-    const int jr_ = j + r;
-    rho[r] = (EDGE && !DIR && (jr_ == 0 || jr_ == n - 1)) ? 0.5 : 1.0;
-    rbnd[r] = EDGE && DIR && (jr_ == 0 || jr_ == n - 1);
-  }
-  // loads: column i of row j-1+a of plane kk at xrow + kk*nn + a*n; a plane
-  // outside the domain / chunk, an eliminated face or an invalid lane reads
-  // the zero page instead (no branches, the load ring stays in place)
-  const double* xrow = xp + (int64_t)(j - 1) * n + i;
-  const double* zpage = g_zero_page + lane;
-  const int obase = j * n + i;  // output (plane 0, row j, column i); int32 offsets (n^3 < 2^31)
-  const bool lane_dbnd = DIR && (i == 0 || i == n - 1);
-
-  auto plane_ok = [&](int kk) { return kk >= 0 && kk < n && !(DIR && (kk == 0 || kk == n - 1)); };
-  double q[3][NR];
-  auto load = [&](int kk, double* v) {
-    const bool pok = colok && kk <= z1 && plane_ok(kk);
-    const double* p = pok ? xrow + kk * (int)nn : zpage;
-#pragma unroll
-    for (int a = 0; a < NR; ++a) v[a] = (!EDGE || rowok[a]) ? __ldg(p + a * n) : 0.0;
-  };
-  // L2 prefetch pd planes ahead: lane a < NR issues one bulk prefetch of its
-  // row's 32-column segment (no registers held; the register loads two
-  // planes ahead then hit L2)
-  const int i0 = i - lane;  // first column of the warp (halo lane)
-  const int pj = j - 1 + lane;
-  const int c_lo = i0 < 0 ? 0 : i0, c_hi = i0 + 32 > n ? n : i0 + 32;
-  const bool pf_lane = pd > 0 && lane < NR && pj >= 0 && pj < n && c_hi > c_lo;
-  const uint64_t pf_a = pf_lane ? reinterpret_cast<uint64_t>(xp + (int64_t)pj * n + c_lo) : 0;
-  const uint64_t pf_b = pf_lane ? reinterpret_cast<uint64_t>(xp + (int64_t)pj * n + c_hi) : 0;
-  auto prefetch = [&](int kk) {
-    if (pf_lane && kk < z1 + 1 && kk < n) {
-      const uint64_t off = (uint64_t)kk * nn * 8;
-      const uint64_t lo = (pf_a + off) & ~(uint64_t)15, hi = (pf_b + off + 15) & ~(uint64_t)15;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
-    }
-  };
-  for (int kk = z0 - 1 + 2; kk < z0 - 1 + 2 + pd; ++kk) prefetch(kk);
-  double U[3][RY], Cc[2][RY];
-#pragma unroll
-  for (int r = 0; r < RY; ++r) U[0][r] = U[1][r] = U[2][r] = Cc[0][r] = Cc[1][r] = 0.0;
-  load(z0 - 1, q[0]);
-  load(z0, q[1]);
-  // step s handles plane k = z0 - 1 + s: U_k, C_k from q[s%3]; emits plane k-1 when k-1 >= z0
-  for (int s0 = 0; z0 - 1 + s0 <= z1; s0 += 6) {
-#pragma unroll
-    for (int u = 0; u < 6; ++u) {
-      const int k = z0 - 1 + s0 + u;
-      if (k > z1) break;
-      prefetch(k + 2 + pd);
-      load(k + 2, q[(u + 2) % 3]);
-      const double* v = q[u % 3];
-      double lr[NR];
-#pragma unroll
-      for (int a = 0; a < NR; ++a)
-        lr[a] = __shfl_up_sync(0xffffffffu, v[a], 1) + __shfl_down_sync(0xffffffffu, v[a], 1);
-      double* Un = U[u % 3];
-      const double* Um = U[(u + 1) % 3];  // U_{k-2}
-      double* Cn = Cc[u % 2];
-      const double* Ck = Cc[(u + 1) % 2];  // C_{k-1}
-      const int ko = k - 1;
-      const bool emit = ko >= z0;
-      const double sig = (!DIR && (ko == 0 || ko == n - 1)) ? 0.5 : 1.0;
-      const bool pbnd = DIR && (ko == 0 || ko == n - 1);
-#pragma unroll
-      for (int r = 0; r < RY; ++r) {
-        const double S = lr[r] + lr[r + 2];
-        const double T = v[r] + v[r + 2];
-        double un = fma(K.b2, T, K.b1 * S);
-        double cn = fma(K.c2, T, K.c1 * S);
-        if (EDGE && !DIR) {
-          un = fma(rho[r], fma(K.b4, v[r + 1], K.b3 * lr[r + 1]), un);
-          cn = fma(rho[r], fma(K.c4, v[r + 1], K.c3 * lr[r + 1]), cn);
-        } else {
-          un = fma(K.b4, v[r + 1], fma(K.b3, lr[r + 1], un));
-          cn = fma(K.c4, v[r + 1], fma(K.c3, lr[r + 1], cn));
-        }
-        if (emit && out_lane && (!EDGE || j + r < n)) {
-          const int o = ko * (int)nn + obase + r * n;
-          double out = DIR ? (Um[r] + un) + Ck[r] : fma(sig, Ck[r], Um[r] + un);
-          if (DIR && (lane_dbnd || rbnd[r] || pbnd)) out = xp[o];
-          if (JAC) out = xp[o] + (omega * (jrp[o] - out)) / dgp[o];
-          yp[o] = out;
-        }
-        Un[r] = un;
-        Cn[r] = cn;
-      }
-    }
-  }
-}
-
-template <int N, int RY, bool JAC>
-__global__ void __launch_bounds__(128) stencil2_kernel(const mdp_problem P, const int32_t* sel,
-                                                        const double* __restrict__ x, int64_t ldx,
-                                                        double* __restrict__ y, int64_t ldy, int zchunk,
-                                                        const double* __restrict__ jr, double omega,
-                                                        const GatherArgs G, int pd) {
-  MDP_PDL_ENTER();
-  const int n = N > 0 ? N : P.n;
-  const int s = sys_of(sel, blockIdx.z);
-  if (G.s_out && blockIdx.y == gridDim.y - 1) {
-    gather_rows(P, s, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5), G.x3, G.x1,
-                ldx, G.s_out);
-    return;
-  }
-  const int lane = threadIdx.x & 31;
-  const int tiles_x = (n + 29) / 30;
-  const int wrow = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int j = (wrow / tiles_x) * RY;
-  if (j >= n) return;
-  const int i = (wrow % tiles_x) * 30 - 1 + lane;
-  const int z0 = blockIdx.y * zchunk;
-  const int z1 = min(n, z0 + zchunk);
-  if (z0 >= n) return;
-  const bool dir = P.bc3d != 0;
-  const Line1D c = make_line(P.h);
-  const int ic = i < 0 ? 0 : (i >= n ? n - 1 : i);
-  const double half = (!dir && (ic == 0 || ic == n - 1)) ? 0.5 : 1.0;
-  const StencilCoef K = stencil_coef(c, P.k_omega, P.sigma_omega, half * c.kd_in, half * c.md_in);
-  const double* xp = x + (int64_t)s * ldx;
-  double* yp = y + (int64_t)s * ldy;
-  const double* jrp = JAC ? jr + (int64_t)s * ldy : nullptr;
-  const double* dgp = JAC ? P.diag_c + (int64_t)s * ldy : nullptr;
-  // edge: a loaded row outside the domain or on an eliminated face
-  const int lo = dir ? 1 : 0, hi = dir ? n - 2 : n - 1;
-  const bool edge = (j - 1 < lo) || (j + RY > hi);
-  if (dir) {
-    if (edge)
-      stencil2_body<N, RY, JAC, true, true>(P, xp, yp, jrp, dgp, omega, n, i, j, z0, z1, K, pd);
-    else
-      stencil2_body<N, RY, JAC, true, false>(P, xp, yp, jrp, dgp, omega, n, i, j, z0, z1, K, pd);
-  } else {
-    if (edge)
-      stencil2_body<N, RY, JAC, false, true>(P, xp, yp, jrp, dgp, omega, n, i, j, z0, z1, K, pd);
-    else
-      stencil2_body<N, RY, JAC, false, false>(P, xp, yp, jrp, dgp, omega, n, i, j, z0, z1, K, pd);
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -799,65 +620,6 @@ static int env_int(const char* name, int dflt) {
 }
 
 template <int N, int RY>
-static void launch_stencil2_t(dim3 grid, cudaStream_t st, const mdp_problem* p, const int32_t* sel, const double* x,
-                              int64_t ldx, double* y, int64_t ldy, int zchunk, const double* jr, double omega,
-                              const GatherArgs& G, int pd) {
-  if (jr)
-    ::mdp::launch_k(stencil2_kernel<N, RY, true>, grid, 128, 0, st, *p, sel, x, ldx, y, ldy, zchunk, jr, omega, G,
-                    pd);
-  else
-    ::mdp::launch_k(stencil2_kernel<N, RY, false>, grid, 128, 0, st, *p, sel, x, ldx, y, ldy, zchunk, jr, omega, G,
-                    pd);
-}
-
-// v2 stencil launch: (x-tile, RY-row group) warps, 4 per block; z-chunks sized
-// so the grid holds ~4 waves of 16 warps per SM, chunks >= 2 planes on small
-// grids (latency-bound) and >= 4 planes otherwise
-static int launch_stencil2(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* x, int64_t ldx,
-                           double* y, int64_t ldy, cudaStream_t st, const double* jr, double omega,
-                           const GatherArgs* g) {
-  const int n = p->n;
-  static const int ry_env = env_int("MDP_STENCIL_RY", 0);  // A/B only
-  const int RY = ry_env == 2 || ry_env == 4 ? ry_env : (n <= 48 ? 2 : 4);
-  const int64_t warps = (int64_t)ceil_div(n, 30) * ceil_div(n, RY);
-  int bx = ceil_div(warps, 4);
-  static const int wave_warps = env_int("MDP_STENCIL_WAVES", 4) * 16;
-  const int64_t want = (int64_t)wave_warps * sm_count();
-  int zch = ceil_div(want, warps * nsel);
-  const int minlen = n <= 48 ? 2 : 4;
-  const int zmax = n / minlen > 1 ? n / minlen : 1;
-  zch = zch < 1 ? 1 : (zch > zmax ? zmax : zch);
-  int zchunk = ceil_div(n, zch);
-  static const int forced = env_int("MDP_STENCIL_ZCHUNK", 0);  // tuning experiments only
-  if (forced > 0) zchunk = forced < n ? forced : n;
-  zch = ceil_div(n, zchunk);
-  const bool gat = g != nullptr && p->qmax > 0;
-  if (gat) bx = bx > ceil_div(p->qmax, 4) ? bx : ceil_div(p->qmax, 4);
-  dim3 grid(bx, zch + (gat ? 1 : 0), nsel);
-  const GatherArgs G = gat ? *g : GatherArgs{nullptr, nullptr, nullptr, 0};
-  static const int pd = env_int("MDP_STENCIL_PD", 6);  // L2 prefetch distance in planes (0: off)
-#define MDP_ST2(NN, R) launch_stencil2_t<NN, R>(grid, st, p, sel, x, ldx, y, ldy, zchunk, jr, omega, G, pd)
-  if (RY == 2) {
-    switch (n) {
-      case 17: MDP_ST2(17, 2); break;
-      case 33: MDP_ST2(33, 2); break;
-      case 129: MDP_ST2(129, 2); break;
-      default: MDP_ST2(0, 2); break;
-    }
-  } else {
-    switch (n) {
-      case 65: MDP_ST2(65, 4); break;
-      case 129: MDP_ST2(129, 4); break;
-      case 193: MDP_ST2(193, 4); break;
-      default: MDP_ST2(0, 4); break;
-    }
-  }
-#undef MDP_ST2
-  MDP_LAUNCH_CHECK("stencil2_kernel");
-  return MDP_OK;
-}
-
-template <int N, int RY>
 static void launch_stencil3_t(dim3 grid, int threads, size_t smem, cudaStream_t st, const mdp_problem* p,
                               const int32_t* sel, const double* x, int64_t ldx, double* y, int64_t ldy, int zchunk,
                               const double* jr, double omega, const GatherArgs& G) {
@@ -932,9 +694,8 @@ static int launch_stencil3(const mdp_problem* p, int32_t nsel, const int32_t* se
 static int launch_stencil(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* x,
                           int64_t ldx, double* y, int64_t ldy, cudaStream_t st, const double* jr = nullptr,
                           double omega = 0.0, const GatherArgs* g = nullptr) {
-  static const int version = env_int("MDP_STENCIL_V", 3);  // 1 / 2: the earlier kernels (A/B)
+  static const int version = env_int("MDP_STENCIL_V", 3);  // 1: the v1 kernel (A/B)
   if (version == 3 && ceil_div(p->n, 32) <= 7) return launch_stencil3(p, nsel, sel, x, ldx, y, ldy, st, jr, omega, g);
-  if (version != 1 && 6 * p->n + 64 <= kZeroPage) return launch_stencil2(p, nsel, sel, x, ldx, y, ldy, st, jr, omega, g);
   const int n = p->n;
   const int64_t warps = (int64_t)ceil_div(n, 30) * ceil_div(n, STENCIL_ROWS);  // (x-tile, row group) per plane
   int bx = ceil_div(warps, 4);
@@ -1015,11 +776,6 @@ extern "C" int mdp_distance_field(int32_t n, const double* seg, int32_t nseg, do
   ::mdp::launch_k(distance_kernel, ceil_div(n3, 256), 256, 0, (cudaStream_t)stream, n, seg, nseg, out);
   MDP_LAUNCH_CHECK("distance_kernel");
   return MDP_OK;
-}
-
-extern "C" int mdp_debug_trace(int on, long long* out) {
-  if (out) return (int)cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));
-  return (int)cudaMemcpyToSymbol(g_trace_on, &on, sizeof(int));
 }
 
 extern "C" int mdp_stencil_apply(const mdp_problem* p, int32_t nsel, const int32_t* sel,

@@ -63,7 +63,7 @@ def child(cases):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--versions", default="1,2")
+    ap.add_argument("--versions", default="1,3")
     ap.add_argument("--cases", default="33x1,65x8,129x1,129x8,193x8")
     ap.add_argument("--env", default="")
     ap.add_argument("--child", action="store_true")
