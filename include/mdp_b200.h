@@ -199,6 +199,20 @@ int mdp_copy_vec(int32_t nsel, const int32_t* sel, const double* src, int64_t ld
  * breakdown, 4 zero rhs -- flagged systems are re-solved by the host path). */
 int mdp_fixed_init(int32_t nsel, int32_t k, const double* beta, double* H, double* cs, double* sn,
                    double* g, double* flag, void* stream);
+/* Fused launches of the same arithmetic (fewer kernels per inner solve):
+ * start  = V0 = b / beta, vcur = V0, and mdp_fixed_init;
+ * arnoldi_givens = mdp_arnoldi followed by mdp_givens_step(j) in its last kernel;
+ * finish = mdp_backsub(m) + x = sum_k y_k Z_k written into x (no fill / copy). */
+int mdp_fixed_start(int32_t nsel, const int32_t* sel, int32_t k, const double* b, int64_t ldb,
+                    const double* beta, double* v0, int64_t ldv, double* vcur, int64_t ldc, int64_t n,
+                    double* H, double* cs, double* sn, double* g, double* flag, void* stream);
+int mdp_arnoldi_givens(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
+                       const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n, double* hcol,
+                       double* vcur, int64_t ldc, void* work, int32_t j, double* H, double* cs, double* sn,
+                       double* g, double* flag, void* stream);
+int mdp_fixed_finish(int32_t nsel, const int32_t* sel, int32_t k, int32_t m, const double* Z, int64_t ldz_sys,
+                     int64_t ldz_vec, double* x, int64_t ldx, int64_t n, double* H, double* g, double* flag,
+                     void* stream);
 int mdp_givens_step(int32_t nsel, int32_t k, int32_t j, const double* hcol, double* H, double* cs,
                     double* sn, double* g, double* flag, void* stream);
 int mdp_backsub(int32_t nsel, int32_t k, int32_t m, const double* H, const double* g,

@@ -65,6 +65,11 @@ _SIGS = {
     "mdp_axpby": (_i32, [_i32, _vp, _f64, _vp, _f64, _vp, _i64, _i64, _vp]),
     "mdp_copy_vec": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
     "mdp_fixed_init": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mdp_fixed_start": (_i32, [_i32, _vp, _i32, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
+                               _vp]),
+    "mdp_arnoldi_givens": (_i32, [_i32, _vp, _vp, _i64, _i64, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _i32,
+                                  _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mdp_fixed_finish": (_i32, [_i32, _vp, _i32, _i32, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "mdp_givens_step": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mdp_backsub": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "mdp_fill": (_i32, [_i32, _vp, _vp, _i64, _i64, _f64, _vp]),

@@ -259,12 +259,21 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
 }
 
 // V[s][nv] = w / hn  (and vcur), exact division like krylov.py:165
+struct GivensArgs {  // optional fused Givens step of the fixed-step inner FGMRES (j = step)
+  int j, k;
+  double *H, *cs, *sn, *g, *flag;
+};
+__device__ __forceinline__ void givens_one(int i, int k, int j, const double* __restrict__ hcol, double* H,
+                                           double* cs, double* sn, double* g, double* flag);
+
 __global__ void arnoldi_next_kernel(const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
                                     const int32_t* __restrict__ nvs, int kmax,
                                     const double* __restrict__ w, int64_t ldw, int64_t n,
-                                    const double* __restrict__ hcol, double* vcur, int64_t ldc) {
+                                    const double* __restrict__ hcol, double* vcur, int64_t ldc,
+                                    const GivensArgs GA) {
   MDP_PDL_ENTER();
   const int i = blockIdx.y;
+  if (GA.H && blockIdx.x == 0 && threadIdx.x == 0) givens_one(i, GA.k, GA.j, hcol, GA.H, GA.cs, GA.sn, GA.g, GA.flag);
   const int s = sys_of(sel, i);
   const int nv = nvs[i];
   const double hn = hcol[i * (kmax + 2) + kmax + 1];
@@ -472,11 +481,8 @@ __global__ void __launch_bounds__(256) ilu0_apply_kernel(const mdp_ilu F, const 
 // per selection index i: H [(k+1) x k] row-major, cs, sn [k], g [k+1].
 // flag: 0 ok, 1 Arnoldi breakdown, 2 lucky breakdown, 4 zero right-hand side
 // (any nonzero flag sends the system through the host-driven exact path).
-__global__ void fixed_init_kernel(int nsel, int k, const double* __restrict__ beta, double* H, double* cs,
-                                  double* sn, double* g, double* flag) {
-  MDP_PDL_ENTER();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nsel) return;
+__device__ __forceinline__ void fixed_init_one(int i, int k, const double* __restrict__ beta, double* H, double* cs,
+                                               double* sn, double* g, double* flag) {
   for (int t = 0; t < (k + 1) * k; ++t) H[(int64_t)i * (k + 1) * k + t] = 0.0;
   for (int t = 0; t < k; ++t) cs[i * k + t] = sn[i * k + t] = 0.0;
   for (int t = 0; t <= k; ++t) g[i * (k + 1) + t] = 0.0;
@@ -484,11 +490,18 @@ __global__ void fixed_init_kernel(int nsel, int k, const double* __restrict__ be
   flag[i] = beta[i] == 0.0 ? 4.0 : 0.0;
 }
 
-__global__ void givens_step_kernel(int nsel, int k, int j, const double* __restrict__ hcol, double* H, double* cs,
-                                   double* sn, double* g, double* flag) {
+__global__ void fixed_init_kernel(int nsel, int k, const double* __restrict__ beta, double* H, double* cs,
+                                  double* sn, double* g, double* flag) {
   MDP_PDL_ENTER();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nsel || flag[i] != 0.0) return;
+  if (i >= nsel) return;
+  fixed_init_one(i, k, beta, H, cs, sn, g, flag);
+}
+
+// one Givens update of system i's Hessenberg column j (krylov.py:142-157)
+__device__ __forceinline__ void givens_one(int i, int k, int j, const double* __restrict__ hcol, double* H,
+                                           double* cs, double* sn, double* g, double* flag) {
+  if (flag[i] != 0.0) return;
   double* Hi = H + (int64_t)i * (k + 1) * k;
   double* c = cs + i * k;
   double* s = sn + i * k;
@@ -515,14 +528,19 @@ __global__ void givens_step_kernel(int nsel, int k, int j, const double* __restr
   if (hn < 1e-14) flag[i] = 2.0;
 }
 
-// y = H[:m,:m]^-1 g[:m] by back substitution (krylov.py:168-171)
-__global__ void backsub_kernel(int nsel, int k, int m, const double* __restrict__ H, const double* __restrict__ g,
-                               const double* __restrict__ flag, double* y) {
+__global__ void givens_step_kernel(int nsel, int k, int j, const double* __restrict__ hcol, double* H, double* cs,
+                                   double* sn, double* g, double* flag) {
   MDP_PDL_ENTER();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nsel) return;
+  givens_one(i, k, j, hcol, H, cs, sn, g, flag);
+}
+
+// y = H[:m,:m]^-1 g[:m] by back substitution (krylov.py:168-171); y = 0 for flagged systems
+__device__ __forceinline__ void backsub_one(int i, int k, int m, const double* __restrict__ H,
+                                            const double* __restrict__ g, const double* __restrict__ flag,
+                                            double* yi) {
   const double* Hi = H + (int64_t)i * (k + 1) * k;
-  double* yi = y + i * k;
   if (flag[i] != 0.0) {
     for (int r = 0; r < k; ++r) yi[r] = 0.0;
     return;
@@ -531,6 +549,61 @@ __global__ void backsub_kernel(int nsel, int k, int m, const double* __restrict_
     double acc = 0.0;
     for (int c = r + 1; c < m; ++c) acc = __dadd_rn(acc, __dmul_rn(Hi[r * k + c], yi[c]));
     yi[r] = __ddiv_rn(__dsub_rn(g[i * (k + 1) + r], acc), Hi[r * k + r]);
+  }
+}
+
+__global__ void backsub_kernel(int nsel, int k, int m, const double* __restrict__ H, const double* __restrict__ g,
+                               const double* __restrict__ flag, double* y) {
+  MDP_PDL_ENTER();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nsel) return;
+  backsub_one(i, k, m, H, g, flag, y + i * k);
+}
+
+// Fused start of the fixed-step inner FGMRES: V0 = b / beta, vcur = V0, and
+// (block 0 of each system) the Hessenberg / Givens state init.  Replaces
+// mdp_scale + mdp_copy_vec + mdp_fixed_init with the same arithmetic.
+struct FixedState {
+  int k;
+  double *H, *cs, *sn, *g, *flag;
+};
+
+__global__ void fixed_start_kernel(const int32_t* sel, const double* __restrict__ b, int64_t ldb,
+                                   const double* __restrict__ beta, double* __restrict__ v0, int64_t ldv,
+                                   double* __restrict__ vcur, int64_t ldc, int64_t n, const FixedState F) {
+  MDP_PDL_ENTER();
+  const int i = blockIdx.y;
+  const int s = sys_of(sel, i);
+  if (blockIdx.x == 0 && threadIdx.x == 0) fixed_init_one(i, F.k, beta, F.H, F.cs, F.sn, F.g, F.flag);
+  const double* bs = b + s * ldb;
+  double* vs = v0 + s * ldv;
+  double* cs = vcur + s * ldc;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = bs[e] / beta[i];
+    vs[e] = v;
+    cs[e] = v;
+  }
+}
+
+// Fused end of the fixed-step inner FGMRES: y = H^-1 g (every block solves the
+// tiny triangular system itself, same order as backsub_kernel), then
+// x = sum_k y_k Z_k written straight into the destination (replaces
+// mdp_backsub + mdp_fill + mdp_basis_update + the copy out).
+__global__ void fixed_finish_kernel(const int32_t* sel, int m, const double* __restrict__ Z, int64_t ldz_sys,
+                                    int64_t ldz_vec, double* __restrict__ x, int64_t ldx, int64_t n,
+                                    const FixedState F) {
+  MDP_PDL_ENTER();
+  __shared__ double ysh[64];
+  const int i = blockIdx.y;
+  const int s = sys_of(sel, i);
+  if (threadIdx.x == 0) backsub_one(i, F.k, m, F.H, F.g, F.flag, ysh);
+  __syncthreads();
+  const double* Zs = Z + s * ldz_sys;
+  double* xs = x + s * ldx;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (int k = 0; k < m; ++k) t += __ldg(Zs + k * ldz_vec + e) * ysh[k];
+    xs[e] = 0.0 + t;  // as fill(0) followed by basis_update's x += t
   }
 }
 
@@ -592,10 +665,30 @@ extern "C" size_t mdp_arnoldi_work_bytes(int32_t nsel, int32_t kmax, int64_t n) 
   return d * sizeof(double) + ((size_t)nsel * sizeof(unsigned int) + 255) / 256 * 256 + 256;
 }
 
+static int arnoldi_impl(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
+                        const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n, double* hcol,
+                        double* vcur, int64_t ldc, void* work, void* stream, const GivensArgs& GA);
+
 extern "C" int mdp_arnoldi(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys,
                            int64_t ldv_vec, const int32_t* nv, int32_t kmax, double* w, int64_t ldw,
                            int64_t n, double* hcol, double* vcur, int64_t ldc, void* work,
                            void* stream) {
+  return arnoldi_impl(nsel, sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n, hcol, vcur, ldc, work, stream,
+                      GivensArgs{0, 0, nullptr, nullptr, nullptr, nullptr, nullptr});
+}
+
+extern "C" int mdp_arnoldi_givens(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
+                                  const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n,
+                                  double* hcol, double* vcur, int64_t ldc, void* work, int32_t j, double* H,
+                                  double* cs, double* sn, double* g, double* flag, void* stream) {
+  MDP_REQUIRE(H && cs && sn && g && flag && j >= 0 && j < kmax, "fused Givens step needs the fixed-step state");
+  return arnoldi_impl(nsel, sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n, hcol, vcur, ldc, work, stream,
+                      GivensArgs{j, kmax, H, cs, sn, g, flag});
+}
+
+static int arnoldi_impl(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
+                        const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n, double* hcol,
+                        double* vcur, int64_t ldc, void* work, void* stream, const GivensArgs& GA) {
   MDP_REQUIRE(kmax >= 1 && kmax <= 63, "kmax %d outside [1, 63]", kmax);
   MDP_REQUIRE(n > 0, "empty vectors");
   MDP_REQUIRE(((uintptr_t)V | (uintptr_t)w) % 16 == 0 && (ldv_sys | ldv_vec | ldw) % 2 == 0,
@@ -630,7 +723,7 @@ extern "C" int mdp_arnoldi(int32_t nsel, const int32_t* sel, double* V, int64_t 
                         pstride, W.ticket, R);
   MDP_LAUNCH_CHECK("orth_pass UPD_NORM");
   ::mdp::launch_k(arnoldi_next_kernel, ew_grid(n, nsel), 256, 0, st, sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n,
-                                                         hcol, vcur, ldc);
+                                                         hcol, vcur, ldc, GA);
   MDP_LAUNCH_CHECK("mdp_arnoldi");
   return MDP_OK;
 }
@@ -704,6 +797,27 @@ extern "C" int mdp_copy_vec(int32_t nsel, const int32_t* sel, const double* src,
   ::mdp::launch_k(copy_vec_kernel, ew_grid(n, nsel), 256, 0, (cudaStream_t)stream, sel, src, lds, dst, ldd, dst_slot,
                                                                       slot_stride, n);
   MDP_LAUNCH_CHECK("mdp_copy_vec");
+  return MDP_OK;
+}
+
+extern "C" int mdp_fixed_start(int32_t nsel, const int32_t* sel, int32_t k, const double* b, int64_t ldb,
+                               const double* beta, double* v0, int64_t ldv, double* vcur, int64_t ldc, int64_t n,
+                               double* H, double* cs, double* sn, double* g, double* flag, void* stream) {
+  if (nsel == 0) return MDP_OK;
+  ::mdp::launch_k(fixed_start_kernel, ew_grid(n, nsel), 256, 0, (cudaStream_t)stream, sel, b, ldb, beta, v0, ldv,
+                  vcur, ldc, n, FixedState{k, H, cs, sn, g, flag});
+  MDP_LAUNCH_CHECK("fixed_start_kernel");
+  return MDP_OK;
+}
+
+extern "C" int mdp_fixed_finish(int32_t nsel, const int32_t* sel, int32_t k, int32_t m, const double* Z,
+                                int64_t ldz_sys, int64_t ldz_vec, double* x, int64_t ldx, int64_t n,
+                                double* H, double* g, double* flag, void* stream) {
+  MDP_REQUIRE(m >= 0 && m <= k && k <= 64, "fixed-step finish: m %d, k %d", m, k);
+  if (nsel == 0) return MDP_OK;
+  ::mdp::launch_k(fixed_finish_kernel, ew_grid(n, nsel), 256, 0, (cudaStream_t)stream, sel, m, Z, ldz_sys, ldz_vec,
+                  x, ldx, n, FixedState{k, H, nullptr, nullptr, g, flag});
+  MDP_LAUNCH_CHECK("fixed_finish_kernel");
   return MDP_OK;
 }
 

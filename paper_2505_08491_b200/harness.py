@@ -143,9 +143,7 @@ class CoupledSolver:
                                          n3, _ext.stream()))
         self.cpl.minus_w_m01(Z, self.b3, sel)
         P = self.inner.apply_device if self.inner is not None else None
-        self.fixed.run(self.C.matvec, P, self.b3, sel, idx)
-        _ext.check(self.lib.mdp_copy_vec(m, sel.data_ptr(), self.fixed.x.data_ptr(), p.ld, Z.data_ptr(), p.ld,
-                                         None, 0, n3, _ext.stream()))
+        self.fixed.run(self.C.matvec, P, self.b3, sel, idx, out=Z)  # z0 written straight into Z[:, :n3]
         flag[:m].copy_(self.fixed.flag[:m])
 
     def solve(self, F=None):

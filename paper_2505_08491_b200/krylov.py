@@ -527,18 +527,21 @@ class FixedStepFgmres:
         wb = self.lib.mdp_arnoldi_work_bytes(nsys, m, n)
         self.work = torch.zeros(wb // 8 + 1, **f)  # reduction tickets must start at zero
 
-    def run(self, A, P, b, sel, idx):
-        """Enqueue the solve of A x = b for the selected systems (no host sync)."""
+    def run(self, A, P, b, sel, idx, out=None):
+        """Enqueue the solve of A x = b for the selected systems (no host sync).
+
+        ``out``: optional (nsys, ld) storage that receives x directly (else self.x).
+        The start, each Arnoldi step's Givens update and the end are fused
+        launches (mdp_fixed_start / mdp_arnoldi_givens / mdp_fixed_finish) with
+        the arithmetic of the separate kernels."""
         L, st = self.lib, _ext.stream()
         m, k, ld, n = int(sel.numel()), self.k, self.ld, self.n
         sp_ = sel.data_ptr()
         _ext.check(L.mdp_norms(m, sp_, b.data_ptr(), ld, n, self.beta.data_ptr(), self.work.data_ptr(), st))
-        _ext.check(L.mdp_fixed_init(m, k, self.beta.data_ptr(), self.H.data_ptr(), self.cs.data_ptr(),
-                                    self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), st))
         V0 = self.V[:, 0, :]
-        _ext.check(L.mdp_scale(m, sp_, b.data_ptr(), ld, None, self.beta.data_ptr(), V0.data_ptr(), (k + 1) * ld, n,
-                               st))
-        _ext.check(L.mdp_copy_vec(m, sp_, V0.data_ptr(), (k + 1) * ld, self.vcur.data_ptr(), ld, None, 0, n, st))
+        _ext.check(L.mdp_fixed_start(m, sp_, k, b.data_ptr(), ld, self.beta.data_ptr(), V0.data_ptr(), (k + 1) * ld,
+                                     self.vcur.data_ptr(), ld, n, self.H.data_ptr(), self.cs.data_ptr(),
+                                     self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), st))
         for j in range(k):
             if P is None:
                 _ext.check(L.mdp_copy_vec(m, sp_, self.vcur.data_ptr(), ld, self.zcur.data_ptr(), ld, None, 0, n, st))
@@ -547,16 +550,13 @@ class FixedStepFgmres:
             Zj = self.Z[:, j, :]
             _ext.check(L.mdp_copy_vec(m, sp_, self.zcur.data_ptr(), ld, Zj.data_ptr(), k * ld, None, 0, n, st))
             A(self.zcur, self.w, sel)
-            _ext.check(L.mdp_arnoldi(m, sp_, self.V.data_ptr(), (k + 1) * ld, ld, self.nvs[j].data_ptr(), k,
-                                     self.w.data_ptr(), ld, n, self.hcol.data_ptr(), self.vcur.data_ptr(), ld,
-                                     self.work.data_ptr(), st))
-            _ext.check(L.mdp_givens_step(m, k, j, self.hcol.data_ptr(), self.H.data_ptr(), self.cs.data_ptr(),
-                                         self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), st))
-        _ext.check(L.mdp_backsub(m, k, k, self.H.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(),
-                                 self.y.data_ptr(), st))
-        _ext.check(L.mdp_fill(m, sp_, self.x.data_ptr(), ld, n, 0.0, st))
-        _ext.check(L.mdp_basis_update(m, sp_, self.x.data_ptr(), ld, self.Z.data_ptr(), k * ld, ld,
-                                      self.cnt.data_ptr(), self.y.data_ptr(), k, n, st))
+            _ext.check(L.mdp_arnoldi_givens(m, sp_, self.V.data_ptr(), (k + 1) * ld, ld, self.nvs[j].data_ptr(), k,
+                                            self.w.data_ptr(), ld, n, self.hcol.data_ptr(), self.vcur.data_ptr(), ld,
+                                            self.work.data_ptr(), j, self.H.data_ptr(), self.cs.data_ptr(),
+                                            self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), st))
+        x = self.x if out is None else out
+        _ext.check(L.mdp_fixed_finish(m, sp_, k, k, self.Z.data_ptr(), k * ld, ld, x.data_ptr(), ld, n,
+                                      self.H.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), st))
 
 
 # ---------------------------------------------------------------------------
