@@ -230,3 +230,52 @@ def test_solve_coupled_direct_1d_vs_reference(gpu, label):
     assert rep.rel_residual <= 1e-6
     assert np.linalg.norm(u3 - g[f"solve_{label}_u3"]) <= 1e-5 * np.linalg.norm(g[f"solve_{label}_u3"])
     assert np.linalg.norm(u1 - g[f"solve_{label}_u1"]) <= 1e-5 * np.linalg.norm(g[f"solve_{label}_u1"])
+
+
+@pytest.mark.parametrize("speculative", [True, False])
+def test_shipped_init_breakdown_path_vs_oracle(gpu, speculative):
+    """The reference's shipped init (head2 = 0, neural.py:413-414) makes the CNN output exactly 0,
+    so every inner FGMRES step breaks down: the graph step flags every system and
+    the exact host path redoes it.  With and without the speculative outer step the reports must
+    equal the oracle's (iterations, breakdowns, history)."""
+    import oracle
+    from oracle import problem as OP
+    from paper_2505_08491_b200 import assembly as A, geometry as G, harness, neural
+    graph = G.Graph1D([[0.5, 0.5, 0.1], [0.5, 0.5, 0.9]], [[0, 1]], 0.02, (0,))
+    s = A.assemble_coupled_system(G.StructuredGrid(17), graph, A.PhysicalParams(epsilon=0.02, beta=1.0),
+                                  n_circle=8, elems_per_edge=32)
+    o = OP.assemble_coupled_system(OP.StructuredGrid(17), OP.segment_graph([0.5, 0.5, 0.1], [0.5, 0.5, 0.9], 0.02),
+                                   OP.PhysicalParams(epsilon=0.02, beta=1.0), n_circle=8, elems_per_edge=32)
+    st = harness.CoupledStrategy(tol=1e-6, maxit=40, restart=30, inner_iterations=3,
+                                 three_d={"type": "neural", "params": neural.init_unet_params(0)})
+    solver = harness.CoupledSolver([s], st)
+    solver.outer.speculative = speculative
+    rep = solver.solve()[0]
+    ost = oracle.CoupledStrategy(tol=1e-6, maxit=40, restart=30, inner_iterations=3,
+                                 three_d={"type": "neural", "params": oracle.init_unet_params(0)})
+    _, _, orep = oracle.solve_coupled(o, ost)
+    assert rep.iterations == orep.iterations
+    assert rep.breakdowns == orep.breakdowns
+    assert rep.converged == orep.converged
+    assert np.allclose(rep.residual_history, orep.residual_history, rtol=1e-8, atol=1e-14)
+
+
+@pytest.mark.parametrize("speculative", [True, False])
+def test_speculative_step_batched_cycle_ends(gpu, speculative):
+    """Three systems with different cycle ends (restart 7 against the stagnating smoothed CNN):
+    speculation on and off give bitwise-identical histories."""
+    from paper_2505_08491_b200 import assembly as A, geometry as G, harness, neural
+    grid = G.StructuredGrid(17)
+    systems = [A.assemble_coupled_system(grid, G.random_tree(4 + 2 * i, 50 + i, 0.02),
+                                         A.PhysicalParams(epsilon=0.02, beta=1.0 + 0.5 * i), elems_per_edge=8)
+               for i in range(3)]
+    out = []
+    for spec_on in (speculative, not speculative):
+        st = harness.CoupledStrategy(tol=1e-9, maxit=25, restart=7, inner_iterations=3,
+                                     three_d={"type": "neural", "params": neural.perturbed_params(1),
+                                              "smoothing": {"maxit": 2}})
+        solver = harness.CoupledSolver(systems, st)
+        solver.outer.speculative = spec_on
+        reps = solver.solve()
+        out.append([(reps[i].iterations, reps[i].breakdowns, list(reps[i].residual_history)) for i in range(3)])
+    assert out[0] == out[1]
