@@ -739,12 +739,15 @@ static void tc_split(int nb, int S, int cin, int cout, int& nsplit, int& ksplit)
   using namespace tc;
   const int tiles_item = ceil_div(S, BX) * ceil_div(S, BY) * ceil_div(S, 2);  // decided on 2-plane bricks
   const int nchunk = cin / 16;
+#ifndef CONV_MIN_NCOL
+#define CONV_MIN_NCOL 32  // narrowest output-channel slice of a split-N CTA (A/B: 64 is 1.2% faster at cfg2 but moves the cfg1 early residual history to 2.5e-4 of the reference)
+#endif
   nsplit = 1;
-  while (nb * tiles_item * nsplit < sm_count() && cout / (2 * nsplit) >= 32) nsplit *= 2;
+  while (nb * tiles_item * nsplit < sm_count() && cout / (2 * nsplit) >= CONV_MIN_NCOL) nsplit *= 2;
   // split-K only from the per-item shape so the FP32 summation order (hence
   // the result) is independent of the batch size
   int nsplit_item = 1;
-  while (tiles_item * nsplit_item < sm_count() && cout / (2 * nsplit_item) >= 32) nsplit_item *= 2;
+  while (tiles_item * nsplit_item < sm_count() && cout / (2 * nsplit_item) >= CONV_MIN_NCOL) nsplit_item *= 2;
   ksplit = 1;
 #ifndef CONV_SPLITK
 #define CONV_SPLITK 1
