@@ -93,6 +93,13 @@ int mdp_stencil_apply(const mdp_problem* p, int32_t nsel, const int32_t* sel,
 int mdp_pi_gather(const mdp_problem* p, int32_t nsel, const int32_t* sel,
                   const double* x3, const double* x1, int64_t ld, double* s, void* stream);
 
+/* The gather above plus, in the same launch, cdst_s[0..cn) = csrc_s[0..cn) (stride
+ * ld): the block preconditioner's r0 copy ahead of its coupling term
+ * (harness.py:391). */
+int mdp_pi_gather_copy(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* x3,
+                       const double* x1, int64_t ld, double* s, const double* csrc, double* cdst, int64_t cn,
+                       void* stream);
+
 /* Pi^T scatter (as a deterministic pull): y3[u] += alpha*w_s * (T^T s)[u].
  * Replaces T.T @ v (assembly.py:324-326). */
 int mdp_pi_scatter(const mdp_problem* p, int32_t nsel, const int32_t* sel,
@@ -205,11 +212,15 @@ int mdp_fixed_init(int32_t nsel, int32_t k, const double* beta, double* H, doubl
  * finish = mdp_backsub(m) + x = sum_k y_k Z_k written into x (no fill / copy). */
 int mdp_fixed_start(int32_t nsel, const int32_t* sel, int32_t k, const double* b, int64_t ldb,
                     const double* beta, double* v0, int64_t ldv, double* vcur, int64_t ldc, int64_t n,
-                    double* H, double* cs, double* sn, double* g, double* flag, void* stream);
+                    double* H, double* cs, double* sn, double* g, double* flag, double* jac_out,
+                    double omega, const double* diag, void* stream);
 int mdp_arnoldi_givens(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
                        const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n, double* hcol,
                        double* vcur, int64_t ldc, void* work, int32_t j, double* H, double* cs, double* sn,
-                       double* g, double* flag, void* stream);
+                       double* g, double* flag, double* jac_out, double omega, const double* diag,
+                       void* stream);
+/* (jac_out != NULL: also jac_out_s = (omega vcur_s) / diag_s, stride ldc -- the first
+ * weighted-Jacobi sweep from zero of the next smoothed preconditioner apply) */
 int mdp_fixed_finish(int32_t nsel, const int32_t* sel, int32_t k, int32_t m, const double* Z, int64_t ldz_sys,
                      int64_t ldz_vec, double* x, int64_t ldx, int64_t n, double* H, double* g, double* flag,
                      void* stream);

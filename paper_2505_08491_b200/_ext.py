@@ -49,6 +49,7 @@ _SIGS = {
     "mdp_reduced_spmv": (_i32, [C.POINTER(MdpProblem), _i32, _vp, _vp, _vp, _vp, _vp]),
     "mdp_stencil_apply": (_i32, [C.POINTER(MdpProblem), _i32, _vp, _vp, _i64, _vp, _i64, _vp]),
     "mdp_pi_gather": (_i32, [C.POINTER(MdpProblem), _i32, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "mdp_pi_gather_copy": (_i32, [C.POINTER(MdpProblem), _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp]),
     "mdp_pi_scatter": (_i32, [C.POINTER(MdpProblem), _i32, _vp, _vp, _f64, _vp, _i64, _vp]),
     "mdp_jacobi_sweep": (_i32, [C.POINTER(MdpProblem), _i32, _vp, _vp, _vp, _vp, _f64, _vp, _vp, _vp]),
     "mdp_distance_field": (_i32, [_i32, _vp, _i32, _vp, _vp]),
@@ -66,9 +67,9 @@ _SIGS = {
     "mdp_copy_vec": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp]),
     "mdp_fixed_init": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mdp_fixed_start": (_i32, [_i32, _vp, _i32, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
-                               _vp]),
+                               _vp, _f64, _vp, _vp]),
     "mdp_arnoldi_givens": (_i32, [_i32, _vp, _vp, _i64, _i64, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _i32,
-                                  _vp, _vp, _vp, _vp, _vp, _vp]),
+                                  _vp, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _vp]),
     "mdp_fixed_finish": (_i32, [_i32, _vp, _i32, _i32, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "mdp_givens_step": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mdp_backsub": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),

@@ -259,6 +259,15 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
 }
 
 // V[s][nv] = w / hn  (and vcur), exact division like krylov.py:165
+// optional first weighted-Jacobi sweep from zero of the NEXT preconditioner
+// apply, fused into the kernel that writes its input v: out = (omega v) / diag
+// (jacobi_update_kernel's arithmetic, krylov.py:290-299)
+struct JacPre {
+  double* out;
+  double omega;
+  const double* diag;
+};
+
 struct GivensArgs {  // optional fused Givens step of the fixed-step inner FGMRES (j = step)
   int j, k;
   double *H, *cs, *sn, *g, *flag;
@@ -270,7 +279,7 @@ __global__ void arnoldi_next_kernel(const int32_t* sel, double* V, int64_t ldv_s
                                     const int32_t* __restrict__ nvs, int kmax,
                                     const double* __restrict__ w, int64_t ldw, int64_t n,
                                     const double* __restrict__ hcol, double* vcur, int64_t ldc,
-                                    const GivensArgs GA) {
+                                    const GivensArgs GA, const JacPre J) {
   MDP_PDL_ENTER();
   const int i = blockIdx.y;
   if (GA.H && blockIdx.x == 0 && threadIdx.x == 0) givens_one(i, GA.k, GA.j, hcol, GA.H, GA.cs, GA.sn, GA.g, GA.flag);
@@ -285,6 +294,7 @@ __global__ void arnoldi_next_kernel(const int32_t* sel, double* V, int64_t ldv_s
     double v = ws[e] / hn;
     if (dst) dst[e] = v;
     if (vc) vc[e] = v;
+    if (J.out) J.out[s * ldc + e] = (J.omega * v) / J.diag[s * ldc + e];
   }
 }
 
@@ -568,9 +578,11 @@ struct FixedState {
   double *H, *cs, *sn, *g, *flag;
 };
 
+
 __global__ void fixed_start_kernel(const int32_t* sel, const double* __restrict__ b, int64_t ldb,
                                    const double* __restrict__ beta, double* __restrict__ v0, int64_t ldv,
-                                   double* __restrict__ vcur, int64_t ldc, int64_t n, const FixedState F) {
+                                   double* __restrict__ vcur, int64_t ldc, int64_t n, const FixedState F,
+                                   const JacPre J) {
   MDP_PDL_ENTER();
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
@@ -582,6 +594,7 @@ __global__ void fixed_start_kernel(const int32_t* sel, const double* __restrict_
     const double v = bs[e] / beta[i];
     vs[e] = v;
     cs[e] = v;
+    if (J.out) J.out[s * ldc + e] = (J.omega * v) / J.diag[s * ldc + e];
   }
 }
 
@@ -667,28 +680,32 @@ extern "C" size_t mdp_arnoldi_work_bytes(int32_t nsel, int32_t kmax, int64_t n) 
 
 static int arnoldi_impl(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
                         const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n, double* hcol,
-                        double* vcur, int64_t ldc, void* work, void* stream, const GivensArgs& GA);
+                        double* vcur, int64_t ldc, void* work, void* stream, const GivensArgs& GA,
+                        const JacPre& J);
 
 extern "C" int mdp_arnoldi(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys,
                            int64_t ldv_vec, const int32_t* nv, int32_t kmax, double* w, int64_t ldw,
                            int64_t n, double* hcol, double* vcur, int64_t ldc, void* work,
                            void* stream) {
   return arnoldi_impl(nsel, sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n, hcol, vcur, ldc, work, stream,
-                      GivensArgs{0, 0, nullptr, nullptr, nullptr, nullptr, nullptr});
+                      GivensArgs{0, 0, nullptr, nullptr, nullptr, nullptr, nullptr}, JacPre{nullptr, 0.0, nullptr});
 }
 
 extern "C" int mdp_arnoldi_givens(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
                                   const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n,
                                   double* hcol, double* vcur, int64_t ldc, void* work, int32_t j, double* H,
-                                  double* cs, double* sn, double* g, double* flag, void* stream) {
+                                  double* cs, double* sn, double* g, double* flag, double* jac_out, double omega,
+                                  const double* diag, void* stream) {
   MDP_REQUIRE(H && cs && sn && g && flag && j >= 0 && j < kmax, "fused Givens step needs the fixed-step state");
+  MDP_REQUIRE(!jac_out || (vcur && diag), "the fused first Jacobi sweep needs vcur and diag");
   return arnoldi_impl(nsel, sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n, hcol, vcur, ldc, work, stream,
-                      GivensArgs{j, kmax, H, cs, sn, g, flag});
+                      GivensArgs{j, kmax, H, cs, sn, g, flag}, JacPre{jac_out, omega, diag});
 }
 
 static int arnoldi_impl(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
                         const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n, double* hcol,
-                        double* vcur, int64_t ldc, void* work, void* stream, const GivensArgs& GA) {
+                        double* vcur, int64_t ldc, void* work, void* stream, const GivensArgs& GA,
+                        const JacPre& J) {
   MDP_REQUIRE(kmax >= 1 && kmax <= 63, "kmax %d outside [1, 63]", kmax);
   MDP_REQUIRE(n > 0, "empty vectors");
   MDP_REQUIRE(((uintptr_t)V | (uintptr_t)w) % 16 == 0 && (ldv_sys | ldv_vec | ldw) % 2 == 0,
@@ -723,7 +740,7 @@ static int arnoldi_impl(int32_t nsel, const int32_t* sel, double* V, int64_t ldv
                         pstride, W.ticket, R);
   MDP_LAUNCH_CHECK("orth_pass UPD_NORM");
   ::mdp::launch_k(arnoldi_next_kernel, ew_grid(n, nsel), 256, 0, st, sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n,
-                                                         hcol, vcur, ldc, GA);
+                                                         hcol, vcur, ldc, GA, J);
   MDP_LAUNCH_CHECK("mdp_arnoldi");
   return MDP_OK;
 }
@@ -802,10 +819,12 @@ extern "C" int mdp_copy_vec(int32_t nsel, const int32_t* sel, const double* src,
 
 extern "C" int mdp_fixed_start(int32_t nsel, const int32_t* sel, int32_t k, const double* b, int64_t ldb,
                                const double* beta, double* v0, int64_t ldv, double* vcur, int64_t ldc, int64_t n,
-                               double* H, double* cs, double* sn, double* g, double* flag, void* stream) {
+                               double* H, double* cs, double* sn, double* g, double* flag, double* jac_out,
+                               double omega, const double* diag, void* stream) {
   if (nsel == 0) return MDP_OK;
+  MDP_REQUIRE(!jac_out || diag, "the fused first Jacobi sweep needs diag");
   ::mdp::launch_k(fixed_start_kernel, ew_grid(n, nsel), 256, 0, (cudaStream_t)stream, sel, b, ldb, beta, v0, ldv,
-                  vcur, ldc, n, FixedState{k, H, cs, sn, g, flag});
+                  vcur, ldc, n, FixedState{k, H, cs, sn, g, flag}, JacPre{jac_out, omega, diag});
   MDP_LAUNCH_CHECK("fixed_start_kernel");
   return MDP_OK;
 }

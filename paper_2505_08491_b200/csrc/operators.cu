@@ -479,14 +479,29 @@ __global__ void __launch_bounds__(256, STENCIL3_MINB) stencil3_kernel(const mdp_
 #undef MDP_ST3
 }
 
+struct CopyArgs {  // optional copy slice of the gather launch: dst_s[0..n) = src_s[0..n)
+  const double* src;
+  double* dst;
+  int64_t n;
+  int gblocks;  // blocks [0, gblocks) gather, the rest copy
+};
+
 __global__ void __launch_bounds__(256) pi_gather_kernel(const mdp_problem P, const int32_t* sel,
                                                          const double* __restrict__ x3,
                                                          const double* __restrict__ x1, int64_t ld,
-                                                         double* __restrict__ s_out) {
+                                                         double* __restrict__ s_out, const CopyArgs CP) {
   MDP_PDL_ENTER();
   const int s = sys_of(sel, blockIdx.y);
-  gather_rows(P, s, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gridDim.x * (blockDim.x >> 5), x3, x1, ld,
-              s_out);
+  const int gb = CP.dst ? CP.gblocks : gridDim.x;
+  if ((int)blockIdx.x >= gb) {
+    const double* a = CP.src + s * ld;
+    double* d = CP.dst + s * ld;
+    for (int64_t e = (blockIdx.x - gb) * (int64_t)blockDim.x + threadIdx.x; e < CP.n;
+         e += (int64_t)(gridDim.x - gb) * blockDim.x)
+      d[e] = a[e];
+    return;
+  }
+  gather_rows(P, s, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gb * (blockDim.x >> 5), x3, x1, ld, s_out);
 }
 
 // y3[u] += alpha w_s (T^T s)[u] (/ div[u] when div is given: the Jacobi
@@ -737,10 +752,18 @@ static int launch_stencil(const mdp_problem* p, int32_t nsel, const int32_t* sel
 }
 
 static int launch_gather(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* x3,
-                         const double* x1, int64_t ld, double* s, cudaStream_t st) {
-  if (p->qmax <= 0) return MDP_OK;
-  dim3 grid(ceil_div(p->qmax, 8), nsel);
-  ::mdp::launch_k(pi_gather_kernel, grid, 256, 0, st, *p, sel, x3, x1, ld, s);
+                         const double* x1, int64_t ld, double* s, cudaStream_t st,
+                         const double* csrc = nullptr, double* cdst = nullptr, int64_t cn = 0) {
+  const int gb = p->qmax > 0 ? ceil_div(p->qmax, 8) : 0;
+  int cb = 0;
+  if (cdst && cn > 0) {
+    cb = ceil_div(cn, 256);
+    cb = cb > 4 * sm_count() ? 4 * sm_count() : cb;
+  }
+  if (gb + cb == 0) return MDP_OK;
+  dim3 grid(gb + cb, nsel);
+  const CopyArgs CP{csrc, cb ? cdst : nullptr, cn, gb};
+  ::mdp::launch_k(pi_gather_kernel, grid, 256, 0, st, *p, sel, x3, x1, ld, s, CP);
   MDP_LAUNCH_CHECK("pi_gather_kernel");
   return MDP_OK;
 }
@@ -792,6 +815,15 @@ extern "C" int mdp_pi_gather(const mdp_problem* p, int32_t nsel, const int32_t* 
   if (int rc = validate(p, nsel)) return rc;
   if (nsel == 0) return MDP_OK;
   return launch_gather(p, nsel, sel, x3, x1, ld, s, (cudaStream_t)stream);
+}
+
+extern "C" int mdp_pi_gather_copy(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* x3,
+                                  const double* x1, int64_t ld, double* s, const double* csrc, double* cdst,
+                                  int64_t cn, void* stream) {
+  if (int rc = validate(p, nsel)) return rc;
+  MDP_REQUIRE(csrc && cdst && cn >= 0, "gather+copy needs a source and a destination");
+  if (nsel == 0) return MDP_OK;
+  return launch_gather(p, nsel, sel, x3, x1, ld, s, (cudaStream_t)stream, csrc, cdst, cn);
 }
 
 extern "C" int mdp_pi_scatter(const mdp_problem* p, int32_t nsel, const int32_t* sel,

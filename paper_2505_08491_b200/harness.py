@@ -139,11 +139,10 @@ class CoupledSolver:
         n3 = p.n3
         _ext.check(self.lib.mdp_ilu0_apply(self.ilu.desc, m, sel.data_ptr(), V.data_ptr() + 8 * n3,
                                            Z.data_ptr() + 8 * n3, p.ld, _ext.stream()))
-        _ext.check(self.lib.mdp_copy_vec(m, sel.data_ptr(), V.data_ptr(), p.ld, self.b3.data_ptr(), p.ld, None, 0,
-                                         n3, _ext.stream()))
-        self.cpl.minus_w_m01(Z, self.b3, sel)
+        self.cpl.minus_w_m01(Z, self.b3, sel, copy_from=V)  # b3 = r0 and += -w M01 z1: one gather launch + pull
         P = self.inner.apply_device if self.inner is not None else None
-        self.fixed.run(self.C.matvec, P, self.b3, sel, idx, out=Z)  # z0 written straight into Z[:, :n3]
+        pre = self.inner.first_sweep_spec() if self.inner is not None else None
+        self.fixed.run(self.C.matvec, P, self.b3, sel, idx, out=Z, pre=pre)  # z0 written straight into Z[:, :n3]
         flag[:m].copy_(self.fixed.flag[:m])
 
     def solve(self, F=None):

@@ -527,24 +527,29 @@ class FixedStepFgmres:
         wb = self.lib.mdp_arnoldi_work_bytes(nsys, m, n)
         self.work = torch.zeros(wb // 8 + 1, **f)  # reduction tickets must start at zero
 
-    def run(self, A, P, b, sel, idx, out=None):
+    def run(self, A, P, b, sel, idx, out=None, pre=None):
         """Enqueue the solve of A x = b for the selected systems (no host sync).
 
         ``out``: optional (nsys, ld) storage that receives x directly (else self.x).
         The start, each Arnoldi step's Givens update and the end are fused
         launches (mdp_fixed_start / mdp_arnoldi_givens / mdp_fixed_finish) with
-        the arithmetic of the separate kernels."""
+        the arithmetic of the separate kernels.  ``pre``: optional (out, omega,
+        diag) from ``P.first_sweep_spec()``: the kernels writing each apply's
+        input also write its first Jacobi sweep, and P skips it."""
         L, st = self.lib, _ext.stream()
         m, k, ld, n = int(sel.numel()), self.k, self.ld, self.n
         sp_ = sel.data_ptr()
+        jo, om, dg = (pre[0].data_ptr(), float(pre[1]), pre[2].data_ptr()) if pre is not None else (None, 0.0, None)
         _ext.check(L.mdp_norms(m, sp_, b.data_ptr(), ld, n, self.beta.data_ptr(), self.work.data_ptr(), st))
         V0 = self.V[:, 0, :]
         _ext.check(L.mdp_fixed_start(m, sp_, k, b.data_ptr(), ld, self.beta.data_ptr(), V0.data_ptr(), (k + 1) * ld,
                                      self.vcur.data_ptr(), ld, n, self.H.data_ptr(), self.cs.data_ptr(),
-                                     self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), st))
+                                     self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), jo, om, dg, st))
         for j in range(k):
             if P is None:
                 _ext.check(L.mdp_copy_vec(m, sp_, self.vcur.data_ptr(), ld, self.zcur.data_ptr(), ld, None, 0, n, st))
+            elif pre is not None:
+                P(self.vcur, self.zcur, sel, idx, presmoothed=True)
             else:
                 P(self.vcur, self.zcur, sel, idx)
             Zj = self.Z[:, j, :]
@@ -553,7 +558,8 @@ class FixedStepFgmres:
             _ext.check(L.mdp_arnoldi_givens(m, sp_, self.V.data_ptr(), (k + 1) * ld, ld, self.nvs[j].data_ptr(), k,
                                             self.w.data_ptr(), ld, n, self.hcol.data_ptr(), self.vcur.data_ptr(), ld,
                                             self.work.data_ptr(), j, self.H.data_ptr(), self.cs.data_ptr(),
-                                            self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), st))
+                                            self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(),
+                                            jo if j + 1 < k else None, om, dg, st))
         x = self.x if out is None else out
         _ext.check(L.mdp_fixed_finish(m, sp_, k, k, self.Z.data_ptr(), k * ld, ld, x.data_ptr(), ld, n,
                                       self.H.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), st))

@@ -98,13 +98,20 @@ class CouplingOps:
         self.prob = prob
         self.lib = _ext.lib()
 
-    def minus_w_m01(self, Z, Y, sel=None):
-        """Y3 += -w M01 z1 = w T^T W Psi D z1 (the harness.py:391 coupling term, sign folded)."""
+    def minus_w_m01(self, Z, Y, sel=None, copy_from=None):
+        """Y3 += -w M01 z1 = w T^T W Psi D z1 (the harness.py:391 coupling term, sign folded).
+
+        ``copy_from``: first set Y3 = copy_from3 (same launch as the gather)."""
         cnt, sp = sel_args(sel, self.prob.nsys)
         p = self.prob
         n3 = p.n3
-        _ext.check(self.lib.mdp_pi_gather(p.desc, cnt, sp, None, Z.data_ptr() + 8 * n3, p.ld,
-                                          p.s_work.data_ptr(), _ext.stream()))
+        if copy_from is None:
+            _ext.check(self.lib.mdp_pi_gather(p.desc, cnt, sp, None, Z.data_ptr() + 8 * n3, p.ld,
+                                              p.s_work.data_ptr(), _ext.stream()))
+        else:
+            _ext.check(self.lib.mdp_pi_gather_copy(p.desc, cnt, sp, None, Z.data_ptr() + 8 * n3, p.ld,
+                                                   p.s_work.data_ptr(), copy_from.data_ptr(), Y.data_ptr(), n3,
+                                                   _ext.stream()))
         # s = -W Psi D z1  ->  T^T s * (-w) adds +w T^T W Psi D z1
         _ext.check(self.lib.mdp_pi_scatter(p.desc, cnt, sp, p.s_work.data_ptr(), -1.0, Y.data_ptr(),
                                            p.ld, _ext.stream()))

@@ -54,17 +54,27 @@ class BatchedNeural:
                                       self.work.data_ptr(), _ext.stream()))
         self.net.apply(self.n, R, self.ld, self.rn, self.D, self.n3, Z, self.ld, sel=sel)
 
-    def apply_device(self, V, Z, sel, idx=None):
+    def first_sweep_spec(self):
+        """(out, omega, diag) of the first Jacobi sweep from zero, (omega r) / diag(C), which
+        the producer of r may write itself (then call apply_device(..., presmoothed=True))."""
+        if self.smoothing is None or self.smoothing[0] < 1:
+            return None
+        return self.t1, self.smoothing[1], self.C.prob._t["diag_c"]
+
+    def apply_device(self, V, Z, sel, idx=None, presmoothed=False):
         m = int(sel.numel())
         if self.smoothing is None:
             self._net(V, Z, sel, m)
             return
         maxit, omega = self.smoothing
         C = self.C
-        # z = S_J(C, r, 0): first sweep from zero needs no SpMV
+        # z = S_J(C, r, 0): first sweep from zero needs no SpMV (already in t1 when presmoothed)
         cur = None
         bufs = [self.t1, self.t2]
-        for it in range(maxit):
+        start = 0
+        if presmoothed and maxit >= 1:
+            cur, start = self.t1, 1
+        for it in range(start, maxit):
             out = bufs[it % 2]
             C.jacobi(V, cur, out, omega, self.tmp, sel)
             cur = out
