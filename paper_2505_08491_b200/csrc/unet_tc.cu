@@ -788,8 +788,12 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   A.cout = cout;
   A.cqc = 4;  // 16-channel chunks: a 46 KB halo per stage leaves room for deep multi-tap weight stages
   A.nchunk = cin / (4 * A.cqc);
-  A.tx = ceil_div(S, BX);
-  A.ty = ceil_div(S, BY);
+  // floor pooling (neural.py:275-290) never reads output plane / row / column
+  // 2*(S/2): pooled layers only compute [0, 2*(S/2))^3 (S = 33: 128 instead of
+  // 255 bricks, one round on 148 SMs); halo loads still see the full input
+  const int Sc = epi == EPI_POOL ? 2 * (S / 2) : S;
+  A.tx = ceil_div(Sc, BX);
+  A.ty = ceil_div(Sc, BY);
   // small layers (few bricks): split the output channels over CTAs (down to
   // 32 per CTA) and, if still short of the SM count, the input chunks
   tc_split(nb, S, cin, cout, A.nsplit, A.ksplit);
@@ -797,8 +801,8 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   // z-tap fold for Cout <= 64 (weights packed [chunk][dydx][quad][dz][Cout][4]);
   // 4-plane bricks when the layer still has >= 2 bricks per SM with them
   A.fold = cout <= 64;
-  const int zp = (A.fold && A.ksplit == 1 && nb * A.tx * A.ty * ceil_div(S, 4) * A.nsplit >= 2 * sm_count()) ? 4 : 2;
-  A.tz = ceil_div(S, zp);
+  const int zp = (A.fold && A.ksplit == 1 && nb * A.tx * A.ty * ceil_div(Sc, 4) * A.nsplit >= 2 * sm_count()) ? 4 : 2;
+  A.tz = ceil_div(Sc, zp);
   const int spatial = nb * A.tx * A.ty * A.tz;
   A.cps = A.nchunk / A.ksplit;
   A.ntiles = spatial * A.nsplit * A.ksplit;
