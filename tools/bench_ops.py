@@ -1,8 +1,8 @@
 """BASELINE config 5: operator microbenchmark sweep (no solve).
 
 Grids n in {33, 65, 129, 193} x batch {1, 8, 64} of seeded 32-segment trees.
-Timed separately (CUDA events, warm, L2 flushed before every timed rep):
-coupled block SpMV, Pi gather, Pi^T scatter (pull), 30-vector Arnoldi
+Timed separately (CUDA events, L2 flushed -- written, then read back -- before
+every timed rep): the K00 stencil alone, the coupled block SpMV, Pi gather, Pi^T scatter (pull), 30-vector Arnoldi
 orthogonalisation, and the CNN preconditioner forward.  Algorithmic bytes /
 FLOPs per SURVEY.md section 8d; peaks from MEASURED_PEAKS.json (HBM) and a
 cuBLAS TF32 GEMM measured in the same run.
@@ -76,6 +76,11 @@ def main():
             Q = prob.Qtot
             U = int(prob._t["u_start"][-1].item())
             r = {"n": n, "batch": nb, "Q_total": Q, "setup_s": round(time.time() - t0, 2)}
+            ms = timed(lambda: ops.stencil(X, Y), a.reps, flush)
+            byt = 16 * n3 * nb
+            r["stencil"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9, "frac_hbm": byt / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                            "frac_hbm_spec_8tbs": byt / (ms * 1e-3) / 8e12, "bytes": byt,
+                            "kernel": "stencil3_kernel (K00 alone)"}
             ms = timed(lambda: A.matvec(X, Y), a.reps, flush)
             byt = sum(16 * x for x in N) + 40 * Q
             r["spmv"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9, "frac_hbm": byt / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
