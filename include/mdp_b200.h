@@ -235,6 +235,22 @@ int mdp_copy_slot(int32_t nsel, const int32_t* sel, const double* src, int64_t l
 int mdp_fill(int32_t nsel, const int32_t* sel, double* y, int64_t ld, int64_t n, double v, void* stream);
 
 /* ------------------------------------------------------------------ */
+/* Geometric multigrid baseline (krylov.py:302-387): the V-cycle pieces on
+ * host-built Galerkin CSR levels (int32 ptr/col, float64 val), one system.   */
+
+/* xo = x + (omega (r - A x)) / d; x == NULL: xo = (omega r) / d (jacobi_smooth, krylov.py:289-299) */
+int mdp_csr_jacobi(int32_t n, const int32_t* ptr, const int32_t* col, const double* val, const double* d,
+                   const double* r, const double* x, double* xo, double omega, void* stream);
+/* res = r - A x */
+int mdp_csr_residual(int32_t n, const int32_t* ptr, const int32_t* col, const double* val, const double* r,
+                     const double* x, double* res, void* stream);
+/* y = A x (accumulate: y += A x) -- also the restriction P^T and prolongation P */
+int mdp_csr_spmv(int32_t n, const int32_t* ptr, const int32_t* col, const double* val, const double* x,
+                 double* y, int32_t accumulate, void* stream);
+/* y = M x, M dense n x n row-major (the inverted coarsest Galerkin matrix) */
+int mdp_dense_matvec(int32_t n, const double* M, const double* x, double* y, void* stream);
+
+/* ------------------------------------------------------------------ */
 /* CNN preconditioner (neural.py:423-472, training.py:290-338).          */
 
 typedef struct mdp_unet {

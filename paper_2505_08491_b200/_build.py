@@ -18,7 +18,7 @@ CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libmdp_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["operators.cu", "krylov.cu", "unet.cu", "unet_tc.cu"]
+CU_SOURCES = ["operators.cu", "krylov.cu", "unet.cu", "unet_tc.cu", "gmg.cu"]
 CPP_SOURCES = ["host.cpp"]
 
 

@@ -52,6 +52,10 @@ _SIGS = {
     "mdp_pi_gather_copy": (_i32, [C.POINTER(MdpProblem), _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp]),
     "mdp_pi_scatter": (_i32, [C.POINTER(MdpProblem), _i32, _vp, _vp, _f64, _vp, _i64, _vp]),
     "mdp_jacobi_sweep": (_i32, [C.POINTER(MdpProblem), _i32, _vp, _vp, _vp, _vp, _f64, _vp, _vp, _vp]),
+    "mdp_csr_jacobi": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _f64, _vp]),
+    "mdp_csr_residual": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mdp_csr_spmv": (_i32, [_i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp]),
+    "mdp_dense_matvec": (_i32, [_i32, _vp, _vp, _vp, _vp]),
     "mdp_distance_field": (_i32, [_i32, _vp, _i32, _vp, _vp]),
     "mdp_ilu0_factor_host": (_i64, [_i64, _vp, _vp, _vp, _vp]),
     "mdp_ilu0_levels_host": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -329,6 +329,12 @@ def host_full_operator(system: CoupledSystem) -> sp.csr_matrix:
                     [w * system.M10, system.K11 + w * system.M11]], format="csr")
 
 
+def host_reduced_operator(system: CoupledSystem) -> sp.csr_matrix:
+    """Assembled host CSR of C = K00 + w M00 (assembly.py:351-353; O(n^3) memory: the
+    geometric-multigrid baseline's Galerkin hierarchy starts from it)."""
+    return (system.K00 + system.params.coupling_weight * system.M00).tocsr()
+
+
 def diag_reduced(system: CoupledSystem) -> np.ndarray:
     """diag(C) = diag(K00) + w diag(M00) without assembling K00 (Kronecker diagonal)."""
     n, h, p = system.grid.n, system.grid.h, system.params

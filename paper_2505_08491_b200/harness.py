@@ -19,9 +19,10 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _ext
-from .assembly import CoupledSystem, DeviceProblem, full_rhs, one_d_operator
+from .assembly import CoupledSystem, DeviceProblem, full_rhs, host_reduced_operator, one_d_operator
 from .geometry import DistanceField, distance_field_device
-from .krylov import DeviceIlu, FgmresEngine, FixedStepFgmres, IluPreconditioner, SolveReport, direct_1d, ilu0
+from .krylov import (DeviceIlu, FgmresEngine, FixedStepFgmres, GmgPreconditioner, IluPreconditioner, SolveReport,
+                     direct_1d, gmg_build, ilu0)
 from .neural import PATH_TCGEN05, UNetParams, device_net, load_checkpoint
 from .operators import CoupledOperator, CouplingOps, ReducedOperator
 from .training import BatchedNeural, NeuralPreconditioner
@@ -44,9 +45,9 @@ class CoupledStrategy:
 def build_preconditioner(spec: dict, grid, C, dfield: DistanceField):
     """Preconditioner factory (harness.py:204-226) for the device path.
 
-    Supported: 'none' and 'neural' (checkpoint path or in-memory
-    ``params``, optional ``smoothing``/``zero_distance``).  The classical
-    baselines (exact / gmg / 3D ilu0) are outside the hot path.
+    Supported: 'none', 'neural' (checkpoint path or in-memory ``params``,
+    optional ``smoothing``/``zero_distance``), the 'gmg' baseline (device
+    V-cycles) and 'ilu0' for small C.  'exact' is outside the device path.
     """
     kind = spec.get("type", "none")
     if kind == "none":
@@ -59,7 +60,36 @@ def build_preconditioner(spec: dict, grid, C, dfield: DistanceField):
                                     zero_distance=spec.get("zero_distance", False))
     if kind == "ilu0" and C is not None and C.shape[0] <= 8000:
         return IluPreconditioner(C)
+    if kind == "gmg":  # the multigrid baseline (harness.py:218-221)
+        levels = spec.get("levels", _default_levels(grid.n))
+        return GmgPreconditioner(gmg_build(grid, C, levels), cycles=spec.get("cycles", 10))
     raise ValueError(f"preconditioner type {kind!r} is not on the device hot path")
+
+
+def _default_levels(n: int) -> int:
+    """harness.py:232-237."""
+    levels = 1
+    while (n - 1) % 2 == 0 and (n - 1) // 2 + 1 >= 3:
+        n = (n - 1) // 2 + 1
+        levels += 1
+    return levels
+
+
+class _BatchedGmg:
+    """Per-system GMG preconditioners behind the batched apply_device interface."""
+
+    def __init__(self, precs, n3):
+        self.precs, self.n3 = precs, n3
+
+    def first_sweep_spec(self):
+        return None
+
+    def apply_device(self, V, Z, sel, idx=None):
+        if idx is None:
+            idx = sel.cpu().tolist()
+        for s in idx:
+            P = self.precs[s]
+            P.hierarchy.device.apply(V[s, :self.n3], Z[s, :self.n3], P.cycles, P.n_pre, P.n_post)
 
 
 def mesh_distance(system: CoupledSystem):
@@ -99,6 +129,10 @@ class CoupledSolver:
             self.inner = BatchedNeural(device_net(params, spec.get("path", path)), dists, p.n, p.ld, p.nsys,
                                        C=self.C, smoothing=smooth,
                                        zero_distance=spec.get("zero_distance", False))
+        elif kind == "gmg":  # the multigrid baseline: one Galerkin hierarchy per system
+            levels = spec.get("levels", _default_levels(p.n))
+            self.inner = _BatchedGmg([GmgPreconditioner(gmg_build(s.grid, host_reduced_operator(s), levels),
+                                                        cycles=spec.get("cycles", 10)) for s in self.systems], p.n3)
         elif kind != "none":
             raise ValueError(f"inner preconditioner {kind!r} is not on the device hot path")
         self.outer = FgmresEngine(p.nsys, p.n3 + p.n1max, p.ld, strategy.restart)

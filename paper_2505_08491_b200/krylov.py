@@ -784,3 +784,208 @@ class IluPreconditioner(Preconditioner):
 
     def apply(self, r):
         return ilu0_apply(self.fact, r)
+
+
+# ---------------------------------------------------------------------------
+# smoothing and geometric multigrid (krylov.py:286-387): the baseline the
+# paper compares the neural preconditioner against ("AMG(m)").  The hierarchy
+# is the reference's own Galerkin construction on the host (scipy products,
+# identical matrices); the V-cycles run on the device (csrc/gmg.cu).
+
+def jacobi_smooth(A, r, x0, maxit: int, omega: float = 2.0 / 3.0):
+    """``maxit`` weighted-Jacobi sweeps on A x = r from x0, host CSR (krylov.py:289-299)."""
+    diag = np.asarray(A.diagonal())
+    if np.any(diag == 0.0):
+        raise ValueError("Jacobi relaxation needs a nonzero diagonal")
+    x = np.array(x0, dtype=float)
+    for _ in range(maxit):
+        x = x + omega * (r - A @ x) / diag
+    return x
+
+
+def prolongation_3d(n_coarse: int) -> sp.csr_matrix:
+    """Trilinear interpolation from an ``n_coarse`` grid to ``2n-1`` points (krylov.py:302-314)."""
+    nf = 2 * n_coarse - 1
+    rows, cols, vals = [], [], []
+    for i in range(nf):
+        if i % 2 == 0:
+            rows.append(i), cols.append(i // 2), vals.append(1.0)
+        else:
+            rows += [i, i]
+            cols += [i // 2, i // 2 + 1]
+            vals += [0.5, 0.5]
+    P1 = sp.csr_matrix((vals, (rows, cols)), shape=(nf, n_coarse))
+    return sp.kron(sp.kron(P1, P1), P1).tocsr()  # x index fastest
+
+
+class _DevCsr:
+    """int32 / float64 CSR arrays of one matrix on the device."""
+
+    def __init__(self, A, device="cuda"):
+        import torch
+        A = sp.csr_matrix(A)
+        A.sort_indices()
+        self.n = A.shape[0]
+        self.ptr = torch.as_tensor(A.indptr.astype(np.int32), device=device)
+        self.col = torch.as_tensor(A.indices.astype(np.int32), device=device)
+        self.val = torch.as_tensor(A.data.astype(np.float64), device=device)
+
+    def args(self):
+        return self.n, self.ptr.data_ptr(), self.col.data_ptr(), self.val.data_ptr()
+
+
+@dataclass
+class GmgHierarchy:
+    """krylov.py:317-322 plus the device copy of every level."""
+
+    matrices: list          # fine to coarse (host CSR)
+    prolongs: list          # prolongs[l]: level l+1 -> level l
+    coarse_lu: object
+    grid_sizes: list
+    device: object = None   # _GmgDevice
+
+
+class _GmgDevice:
+    def __init__(self, hier: GmgHierarchy):
+        import torch
+        self.lib = _ext.lib()
+        self.A = [_DevCsr(M) for M in hier.matrices]
+        self.d = [torch.as_tensor(np.asarray(M.diagonal(), dtype=np.float64), device="cuda") for M in hier.matrices]
+        self.P = [_DevCsr(P) for P in hier.prolongs]
+        self.PT = [_DevCsr(P.T.tocsr()) for P in hier.prolongs]
+        # the coarsest solve (splu in the reference) as a dense inverse: the level has 27-125 unknowns
+        Mc = hier.matrices[-1].toarray()
+        self.Minv = torch.as_tensor(np.linalg.inv(Mc).ravel(), device="cuda")
+        f = dict(dtype=torch.float64, device="cuda")
+        sizes = [M.shape[0] for M in hier.matrices]
+        self.r = [torch.zeros(s, **f) for s in sizes]      # right-hand side per level
+        self.z = [torch.zeros(s, **f) for s in sizes]      # solution per level
+        self.t = [torch.zeros(s, **f) for s in sizes]      # sweep / residual scratch per level
+        self.acc = torch.zeros(sizes[0], **f)
+        self.res0 = torch.zeros(sizes[0], **f)
+
+    def _copy(self, src, dst):
+        _ext.check(self.lib.mdp_copy_vec(1, None, src.data_ptr(), 0, dst.data_ptr(), 0, None, 0, src.numel(),
+                                         _ext.stream()))
+
+    def _sweeps(self, l, r, z, k, omega, from_zero):
+        """k Jacobi sweeps on level l (jacobi_smooth, krylov.py:289-299); the result lands in z,
+        which holds the start vector unless from_zero."""
+        L, st = self.lib, _ext.stream()
+        n, pp, cc, vv = self.A[l].args()
+        if k == 0:
+            if from_zero:
+                _ext.check(L.mdp_fill(1, None, z.data_ptr(), 0, n, 0.0, st))
+            return
+        # ping-pong between z and the level scratch so that the last sweep writes z
+        bufs = (z, self.t[l]) if (from_zero and k % 2 == 1) else (self.t[l], z)
+        cur = None if from_zero else z
+        if not from_zero and k % 2 == 1:
+            self._copy(z, self.t[l])  # odd count from a start vector: start from the scratch copy
+            cur, bufs = self.t[l], (z, self.t[l])
+        for it in range(k):
+            dst = bufs[it % 2]
+            _ext.check(L.mdp_csr_jacobi(n, pp, cc, vv, self.d[l].data_ptr(), r.data_ptr(),
+                                        None if cur is None else cur.data_ptr(), dst.data_ptr(), float(omega), st))
+            cur = dst
+
+    def vcycle(self, l, r, z, n_pre, n_post, omega=2.0 / 3.0):
+        """z = V(r) on level l (krylov.py:343-356)."""
+        L, st = self.lib, _ext.stream()
+        if l == len(self.A) - 1:
+            _ext.check(L.mdp_dense_matvec(self.A[l].n, self.Minv.data_ptr(), r.data_ptr(), z.data_ptr(), st))
+            return
+        self._sweeps(l, r, z, n_pre, omega, from_zero=True)
+        n, pp, cc, vv = self.A[l].args()
+        _ext.check(L.mdp_csr_residual(n, pp, cc, vv, r.data_ptr(), z.data_ptr(), self.t[l].data_ptr(), st))
+        nc, qp, qc, qv = self.PT[l].args()
+        _ext.check(L.mdp_csr_spmv(nc, qp, qc, qv, self.t[l].data_ptr(), self.r[l + 1].data_ptr(), 0, st))
+        self.vcycle(l + 1, self.r[l + 1], self.z[l + 1], n_pre, n_post, omega)
+        nf, fp, fc, fv = self.P[l].args()
+        _ext.check(L.mdp_csr_spmv(nf, fp, fc, fv, self.z[l + 1].data_ptr(), z.data_ptr(), 1, st))
+        self._sweeps(l, r, z, n_post, omega, from_zero=False)
+
+    def apply(self, r, z, cycles, n_pre, n_post):
+        """z = GmgPreconditioner.apply(r) (krylov.py:373-387) on device vectors of the fine size."""
+        L, st = self.lib, _ext.stream()
+        self.vcycle(0, r, z, n_pre, n_post)
+        n, pp, cc, vv = self.A[0].args()
+        for _ in range(cycles - 1):
+            _ext.check(L.mdp_csr_residual(n, pp, cc, vv, r.data_ptr(), z.data_ptr(), self.res0.data_ptr(), st))
+            self.vcycle(0, self.res0, self.acc, n_pre, n_post)
+            # z = z + V(r - A z)  (krylov.py:385-386)
+            _ext.check(L.mdp_axpby(1, None, 1.0, self.acc.data_ptr(), 1.0, z.data_ptr(), 0, n, st))
+
+
+def gmg_build(grid, fine_operator, levels: int) -> GmgHierarchy:
+    """Galerkin hierarchy below a fine operator (krylov.py:325-340), same checks and messages.
+
+    ``fine_operator``: a sparse matrix, a callable grid -> matrix, or this
+    package's device ``reduced_operator`` (assembled on the host here)."""
+    if levels < 1:
+        raise ValueError("levels must be at least 1")
+    if hasattr(fine_operator, "prob") and hasattr(fine_operator, "matvec"):  # device reduced_operator
+        from .assembly import host_reduced_operator
+        A0 = host_reduced_operator(fine_operator.prob.systems[0])
+    elif callable(fine_operator) and not sp.issparse(fine_operator):
+        A0 = fine_operator(grid)
+    else:
+        A0 = fine_operator
+    if A0.shape != (grid.num_nodes, grid.num_nodes):
+        raise ValueError("fine operator shape does not match the grid")
+    mats = [sp.csr_matrix(A0)]
+    prolongs = []
+    sizes = [grid.n]
+    n = grid.n
+    for _ in range(levels - 1):
+        if (n - 1) % 2 != 0 or (n - 1) // 2 + 1 < 3:
+            raise ValueError(f"grid with {n} points per edge is not coarsenable")
+        nc = (n - 1) // 2 + 1
+        P = prolongation_3d(nc)
+        mats.append((P.T @ mats[-1] @ P).tocsr())
+        prolongs.append(P)
+        sizes.append(nc)
+        n = nc
+    import scipy.sparse.linalg as spla
+    coarse_lu = spla.splu(sp.csc_matrix(mats[-1]))
+    hier = GmgHierarchy(mats, prolongs, coarse_lu, sizes)
+    hier.device = _GmgDevice(hier)
+    return hier
+
+
+def gmg_vcycle(hierarchy: GmgHierarchy, r, n_pre: int = 1, n_post: int = 1):
+    """One V-cycle for A z = r with damped-Jacobi smoothing (krylov.py:343-356), on the device."""
+    import torch
+    r = np.asarray(r, dtype=float)
+    dev = hierarchy.device
+    R = torch.as_tensor(r, device="cuda")
+    Z = torch.zeros_like(R)
+    dev.vcycle(0, R, Z, n_pre, n_post)
+    return Z.cpu().numpy()
+
+
+class GmgPreconditioner(Preconditioner):
+    """Fixed number of V-cycles per application, the AMG(m) analogue (krylov.py:359-387)."""
+
+    def __init__(self, hierarchy: GmgHierarchy, cycles: int = 1, n_pre: int = 1, n_post: int = 1):
+        if cycles < 1:
+            raise ValueError("cycles must be at least 1")
+        self.hierarchy = hierarchy
+        self.cycles = cycles
+        self.n_pre = n_pre
+        self.n_post = n_post
+
+    def apply(self, r):
+        import torch
+        R = torch.as_tensor(np.asarray(r, dtype=float), device="cuda")
+        Z = torch.zeros_like(R)
+        self.hierarchy.device.apply(R, Z, self.cycles, self.n_pre, self.n_post)
+        return Z.cpu().numpy()
+
+    def apply_device(self, V, Z, sel, idx=None):
+        """Z_s[:n] = P(V_s[:n]) for the (single) listed system of an (nsys, ld) storage."""
+        if idx is None:
+            idx = sel.cpu().tolist()
+        n = self.hierarchy.matrices[0].shape[0]
+        for s in idx:
+            self.hierarchy.device.apply(V[s, :n], Z[s, :n], self.cycles, self.n_pre, self.n_post)

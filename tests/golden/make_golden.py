@@ -375,8 +375,50 @@ def gen_formats():
          radius=np.array(g.radius), dirichlet=np.array(g.dirichlet_vertices))
 
 
+def gen_gmg():
+    # geometric multigrid baseline (krylov.py:302-387) on reduced operators of two coupled systems
+    out = {}
+    cases = [("n9", geometry.StructuredGrid(9), geometry.generate_graph(geometry.GraphFamilySpec(n_branches=5), 3),
+              assembly.PhysicalParams(), 3)]
+    try:
+        g17 = geometry.Graph1D(np.array([[0.5, 0.5, 0.1], [0.5, 0.5, 0.9]]), np.array([[0, 1]]), 0.02, (0,))
+        cases.append(("n17", geometry.StructuredGrid(17), g17, BetaParams(epsilon=0.02, beta=1.0), 4))
+        for tag, grid, g, params, levels in cases:
+            # cfg1 geometry: 32 elements on the segment (fixed refinement); n9: the reference refinement
+            assembly.refine_graph = fixed_refine(32) if tag == "n17" else _ORIG_REFINE
+            s = assembly.assemble_coupled_system(grid, g, params, n_circle=8 if tag == "n17" else 1)
+            C = assembly.reduced_operator(s).tocsr()
+            hier = krylov.gmg_build(grid, C, levels)
+            rng = np.random.default_rng(31)
+            r = rng.standard_normal(grid.num_nodes)
+            out[f"{tag}_r"] = r
+            out[f"{tag}_vcycle"] = krylov.gmg_vcycle(hier, r)
+            out[f"{tag}_vcycle_22"] = krylov.gmg_vcycle(hier, r, n_pre=2, n_post=2)
+            out[f"{tag}_apply3"] = krylov.GmgPreconditioner(hier, cycles=3).apply(r)
+            b = rng.standard_normal(grid.num_nodes)
+            out[f"{tag}_b"] = b
+            x, rep = krylov.fgmres(C, krylov.GmgPreconditioner(hier, cycles=2), b, restart=20, tol=1e-8, maxit=200)
+            out[f"{tag}_iters"] = np.array(rep.iterations)
+            out[f"{tag}_hist"] = np.array(rep.residual_history)
+            out[f"{tag}_x"] = x
+            out[f"{tag}_coarse_nnz"] = np.array([M.nnz for M in hier.matrices])
+            if tag == "n9":  # coupled solve with the gmg inner preconditioner (harness.py:218-221, 377-387)
+                st = harness.CoupledStrategy(tol=1e-6, maxit=60, restart=30, inner_iterations=3, one_d="ilu0",
+                                             three_d={"type": "gmg", "cycles": 2, "levels": levels})
+                u3, u1, crep = harness.solve_coupled(s, st)
+                out["coupled_iters"] = np.array(crep.iterations)
+                out["coupled_conv"] = np.array(crep.converged)
+                out["coupled_hist"] = np.array(crep.residual_history)
+                out["coupled_u3"] = u3
+                print("gmg coupled", crep.iterations, crep.converged)
+            print("gmg", tag, rep.iterations, rep.converged, [M.shape[0] for M in hier.matrices])
+    finally:
+        assembly.refine_graph = _ORIG_REFINE
+    dump("gmg", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["assembly", "fgmres", "unet", "apply", "cfg1", "direct", "formats"]
+    which = sys.argv[1:] or ["assembly", "fgmres", "unet", "apply", "cfg1", "direct", "formats", "gmg"]
     if "assembly" in which:
         gen_assembly()
     if "fgmres" in which:
@@ -391,3 +433,5 @@ if __name__ == "__main__":
         gen_direct()
     if "formats" in which:
         gen_formats()
+    if "gmg" in which:
+        gen_gmg()

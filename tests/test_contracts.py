@@ -56,4 +56,4 @@ def test_coupled_strategy_contracts():
     with pytest.raises(ValueError):  # 'schur' is not on the device path
         harness.solve_coupled(s, harness.CoupledStrategy(one_d="schur"))
     with pytest.raises(ValueError):
-        harness.build_preconditioner({"type": "gmg"}, s.grid, None, None)
+        harness.build_preconditioner({"type": "exact"}, s.grid, None, None)

@@ -132,3 +132,20 @@ def test_tree_elimination_order_is_fill_free():
     C = sp.csr_matrix(np.array([[2.0, -1, -1], [-1, 2, -1], [-1, -1, 2]]))
     with pytest.raises(ValueError):
         tree_elimination_order(C)
+
+
+def test_gmg_hierarchy_contracts():
+    """prolongation partition of unity, Galerkin products, non-coarsenable grids (reference tests/test_krylov.py)."""
+    from paper_2505_08491_b200 import krylov
+    P = krylov.prolongation_3d(3)
+    assert np.allclose(P @ np.ones(27), 1.0)
+    grid = G.StructuredGrid(9)
+    Kl = A.assemble_3d(grid, A.PhysicalParams(k_omega=1.0, sigma_omega=1.0))
+    P0 = krylov.prolongation_3d(5)
+    assert abs((P0.T @ Kl @ P0) - (P0.T @ Kl @ P0)).max() == 0.0
+    with pytest.raises(ValueError, match="coarsenable"):
+        krylov.gmg_build(G.StructuredGrid(6), A.assemble_3d(G.StructuredGrid(6), A.PhysicalParams()), 2)
+    with pytest.raises(ValueError, match="at least 1"):
+        krylov.gmg_build(grid, Kl, 0)
+    with pytest.raises(ValueError):
+        krylov.GmgPreconditioner(None, cycles=0)
