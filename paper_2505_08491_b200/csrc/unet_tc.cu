@@ -801,7 +801,9 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   // z-tap fold for Cout <= 64 (weights packed [chunk][dydx][quad][dz][Cout][4]);
   // 4-plane bricks when the layer still has >= 2 bricks per SM with them
   A.fold = cout <= 64;
-  const int zp = (A.fold && A.ksplit == 1 && nb * A.tx * A.ty * ceil_div(Sc, 4) * A.nsplit >= 2 * sm_count()) ? 4 : 2;
+  // decided from the per-item shape only (like split-K): the brick depth sets the
+  // FP32 accumulation order, so batched == serial stays bitwise (training.py:322-338)
+  const int zp = (A.fold && A.ksplit == 1 && (int64_t)A.tx * A.ty * ceil_div(Sc, 4) >= 2 * sm_count()) ? 4 : 2;
   A.tz = ceil_div(Sc, zp);
   const int spatial = nb * A.tx * A.ty * A.tz;
   A.cps = A.nchunk / A.ksplit;
