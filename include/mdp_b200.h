@@ -71,6 +71,12 @@ typedef struct mdp_problem {
   const double* p_val;
   const double* diag_c;    /* [nsys*ld] diag(C) for Jacobi (or NULL)        */
   int32_t qmax, umax, r1max, pad1; /* per-system maxima (launch shapes)      */
+  /* optional ELL copy of the pull list: entries of touched node u at
+   * [u*ell_w, (u+1)*ell_w), padded with value 0 (no row-pointer load on the
+   * pull's dependent-load chain); NULL: use u_ptr / u_q / u_val */
+  const int32_t* ell_q;
+  const double* ell_val;
+  int32_t ell_w, pad2;
 } mdp_problem;
 
 /* y = A x, A = [K00 + w M00, w M01; w M10, K11 + w M11]

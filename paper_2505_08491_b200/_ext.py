@@ -29,7 +29,8 @@ class MdpProblem(C.Structure):
                 ("u_start", _vp), ("u_node", _vp), ("u_ptr", _vp), ("u_q", _vp), ("u_val", _vp),
                 ("r1_start", _vp), ("k_ptr", _vp), ("k_col", _vp), ("k_val", _vp),
                 ("p_ptr", _vp), ("p_q", _vp), ("p_val", _vp), ("diag_c", _vp),
-                ("qmax", _i32), ("umax", _i32), ("r1max", _i32), ("pad1", _i32)]
+                ("qmax", _i32), ("umax", _i32), ("r1max", _i32), ("pad1", _i32),
+                ("ell_q", _vp), ("ell_val", _vp), ("ell_w", _i32), ("pad2", _i32)]
 
 
 class MdpIlu(C.Structure):

@@ -18,6 +18,8 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 import scipy.sparse as sp
 
@@ -452,6 +454,22 @@ class DeviceProblem:
             x = np.concatenate(x) if isinstance(x, list) and x and isinstance(x[0], np.ndarray) else np.asarray(x)
             return torch.as_tensor(np.asarray(x, dtype=np.float64).ravel(), device=dev)
 
+        # ELL copy of the pull list (width = widest touched node, a multiple of 8 lanes);
+        # padding entries carry value 0 and the row's first quadrature index
+        up = np.asarray(u_ptr, dtype=np.int64)
+        uq = np.concatenate(u_q) if u_q else np.zeros(0, dtype=np.int32)
+        uv = np.concatenate(u_val) if u_val else np.zeros(0)
+        cnt = np.diff(up)
+        ell_w = int(max(8, -(-int(cnt.max()) // 8) * 8)) if len(cnt) else 8
+        nu = len(cnt)
+        ell_q = np.zeros((max(nu, 1), ell_w), dtype=np.int32)
+        ell_v = np.zeros((max(nu, 1), ell_w))
+        if nu:
+            pos = np.arange(len(uq)) - np.repeat(up[:-1], cnt)
+            row = np.repeat(np.arange(nu), cnt)
+            ell_q[:] = uq[up[:-1]][:, None]
+            ell_q[row, pos] = uq
+            ell_v[row, pos] = uv
         self._t = dict(
             wc=f64([s.params.coupling_weight for s in systems]), n1=i32(self.n1),
             q_start=i32(q_start), t_ptr=i32(t_ptr), t_col=i32(t_col), t_val=f64(t_val),
@@ -462,6 +480,7 @@ class DeviceProblem:
             p_ptr=i32(p_ptr), p_q=i32(p_q if p_q else [np.zeros(0)]),
             p_val=f64(p_val if p_val else [np.zeros(0)]),
             diag_c=torch.as_tensor(diag, device=dev),
+            ell_q=i32(ell_q), ell_val=f64(ell_v),
         )
         self.Qtot = int(q_start[-1])
         P = _ext.MdpProblem()
@@ -472,6 +491,9 @@ class DeviceProblem:
         P.qmax = int(np.max(np.diff(q_start)))
         P.umax = int(np.max(np.diff(u_start))) if len(u_start) > 1 else 0
         P.r1max = int(self.n1.max())
+        P.ell_w = ell_w
+        if os.environ.get("MDP_NO_ELL"):  # A/B only: the CSR pull
+            P.ell_q, P.ell_val = None, None
         self.desc = P
         self.s_work = torch.zeros(max(1, self.Qtot), dtype=torch.float64, device=dev)
         self.ilu = None

@@ -519,7 +519,12 @@ __device__ __forceinline__ void pull_rows(const mdp_problem& P, int s, int g0, i
     const bool live = base < ucount;
     double acc = 0.0;
     if (live)
-      for (int k = P.u_ptr[u] + sub; k < P.u_ptr[u + 1]; k += 8) acc += P.u_val[k] * sv[P.u_q[k]];
+      if (P.ell_q) {  // fixed-width rows: the entry loads depend on u only
+        const int64_t b = (int64_t)u * P.ell_w;
+        for (int k = sub; k < P.ell_w; k += 8) acc += P.ell_val[b + k] * sv[P.ell_q[b + k]];
+      } else {
+        for (int k = P.u_ptr[u] + sub; k < P.u_ptr[u + 1]; k += 8) acc += P.u_val[k] * sv[P.u_q[k]];
+      }
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (live && sub == 0) {
