@@ -410,11 +410,17 @@ __global__ void copy_vec_kernel(const int32_t* sel, const double* __restrict__ s
 // operations (no FMA contraction), so results equal krylov.ilu0_apply
 // bitwise.  The system's factor is first staged in shared memory (when it
 // fits) so each level costs a barrier plus shared-memory latency only.
-__global__ void __launch_bounds__(256) ilu0_apply_kernel(const mdp_ilu F, const int32_t* sel,
-                                                          const double* __restrict__ r,
-                                                          double* __restrict__ z, int64_t ld, int staged) {
+// staged: 1 = factor, schedule and x in shared memory; 0 = x in shared memory;
+// -1 = everything in global memory, x kept in z (the 3D ILU(0) baseline on C,
+// too large for shared memory; L2 reads after each level barrier)
+__global__ void __launch_bounds__(1024) ilu0_apply_kernel(const mdp_ilu F, const int32_t* sel,
+                                                           const double* __restrict__ r,
+                                                           double* __restrict__ z, int64_t ld, int staged) {
   MDP_PDL_ENTER();
-  extern __shared__ double xsh[];
+  extern __shared__ double xsh_[];
+  const bool xglob = staged < 0;
+  if (xglob) staged = 0;
+  double* xsh = xglob ? z + sys_of(sel, blockIdx.x) * ld : xsh_;
   const int s = sys_of(sel, blockIdx.x);
   const int rs = F.row_start[s], nrow = F.row_start[s + 1] - rs;
   const int p0 = F.ptr[rs], nnz = F.ptr[rs + nrow] - p0;
@@ -458,16 +464,20 @@ __global__ void __launch_bounds__(256) ilu0_apply_kernel(const mdp_ilu F, const 
   }
   // x = P r (the forward sweep reads x[row] before writing it)
   const int32_t* gp = F.perm ? F.perm + rs : nullptr;
-  for (int t = threadIdx.x; t < nrow; t += blockDim.x) xsh[t] = rp[gp ? gp[t] : t];
+  if (!xglob)
+    for (int t = threadIdx.x; t < nrow; t += blockDim.x) xsh[t] = rp[gp ? gp[t] : t];
+  else if (rp != xsh)
+    for (int t = threadIdx.x; t < nrow; t += blockDim.x) xsh[t] = rp[t];
   __syncthreads();
   for (int L = 0; L < nlf; ++L) {
     for (int t = levf[L] + threadIdx.x; t < levf[L + 1]; t += blockDim.x) {
       const int row = pf[t];
       const int a = staged ? psh[row] : F.ptr[rs + row] - p0;
       const int d = staged ? dsh[row] : F.diag[rs + row] - p0;
-      double acc = xsh[row];
-      for (int p = a; p < d; ++p) acc = __dsub_rn(acc, __dmul_rn(val[p], xsh[col[p]]));
-      xsh[row] = acc;
+      double acc = xglob ? __ldcg(xsh + row) : xsh[row];
+      for (int p = a; p < d; ++p)
+        acc = __dsub_rn(acc, __dmul_rn(val[p], xglob ? __ldcg(xsh + col[p]) : xsh[col[p]]));
+      if (xglob) __stcg(xsh + row, acc); else xsh[row] = acc;
     }
     __syncthreads();
   }
@@ -476,12 +486,14 @@ __global__ void __launch_bounds__(256) ilu0_apply_kernel(const mdp_ilu F, const 
       const int row = pb[t];
       const int d = staged ? dsh[row] : F.diag[rs + row] - p0;
       const int e = staged ? psh[row + 1] : F.ptr[rs + row + 1] - p0;
-      double acc = xsh[row];
-      for (int p = d + 1; p < e; ++p) acc = __dsub_rn(acc, __dmul_rn(val[p], xsh[col[p]]));
-      xsh[row] = __ddiv_rn(acc, val[d]);
+      double acc = xglob ? __ldcg(xsh + row) : xsh[row];
+      for (int p = d + 1; p < e; ++p)
+        acc = __dsub_rn(acc, __dmul_rn(val[p], xglob ? __ldcg(xsh + col[p]) : xsh[col[p]]));
+      if (xglob) __stcg(xsh + row, __ddiv_rn(acc, val[d])); else xsh[row] = __ddiv_rn(acc, val[d]);
     }
     __syncthreads();
   }
+  if (xglob) return;  // x already is z
   double* zp = z + s * ld;
   for (int t = threadIdx.x; t < nrow; t += blockDim.x) zp[gp ? gp[t] : t] = xsh[t];
 }
@@ -892,13 +904,19 @@ extern "C" int mdp_ilu0_apply(const mdp_ilu* f, int32_t nsel, const int32_t* sel
   const size_t base = (size_t)f->max_rows * sizeof(double);
   const size_t full = base + (size_t)f->max_nnz * (sizeof(double) + sizeof(int)) +
                       (size_t)(4 * f->max_rows + 1 + 2 * f->lev_stride) * sizeof(int);
-  const int staged = full <= cap;
-  MDP_REQUIRE(base <= cap, "1D block of %d rows too large for the single-CTA sweep", f->max_rows);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(ilu0_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
     attr = true;
   }
+  if (base > cap) {  // large (3D) factors: x lives in z, 1024 threads per level
+    MDP_REQUIRE(f->perm == nullptr, "permuted (direct) factors must fit the shared-memory sweep");
+    MDP_REQUIRE(r != z, "the global-memory ILU sweep needs r and z distinct");
+    ::mdp::launch_k(ilu0_apply_kernel, nsel, 1024, 0, (cudaStream_t)stream, *f, sel, r, z, ld, -1);
+    MDP_LAUNCH_CHECK("mdp_ilu0_apply");
+    return MDP_OK;
+  }
+  const int staged = full <= cap;
   ::mdp::launch_k(ilu0_apply_kernel, nsel, 256, staged ? full : base, (cudaStream_t)stream, *f, sel, r, z, ld, staged);
   MDP_LAUNCH_CHECK("mdp_ilu0_apply");
   return MDP_OK;

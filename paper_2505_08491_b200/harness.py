@@ -47,7 +47,8 @@ def build_preconditioner(spec: dict, grid, C, dfield: DistanceField):
 
     Supported: 'none', 'neural' (checkpoint path or in-memory ``params``,
     optional ``smoothing``/``zero_distance``), the 'gmg' baseline (device
-    V-cycles) and 'ilu0' for small C.  'exact' is outside the device path.
+    V-cycles) and 'ilu0' (host factor, device level-scheduled sweeps).  'exact'
+    is outside the device path.
     """
     kind = spec.get("type", "none")
     if kind == "none":
@@ -58,7 +59,7 @@ def build_preconditioner(spec: dict, grid, C, dfield: DistanceField):
         smooth = (sm["maxit"], sm.get("omega", 2.0 / 3.0)) if isinstance(sm, dict) else sm
         return NeuralPreconditioner(params, dfield, smoothing=smooth, C=C,
                                     zero_distance=spec.get("zero_distance", False))
-    if kind == "ilu0" and C is not None and C.shape[0] <= 8000:
+    if kind == "ilu0" and C is not None:
         return IluPreconditioner(C)
     if kind == "gmg":  # the multigrid baseline (harness.py:218-221)
         levels = spec.get("levels", _default_levels(grid.n))

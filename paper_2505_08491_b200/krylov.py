@@ -739,8 +739,6 @@ class DeviceIlu:
         for i, f in enumerate(factors):
             lev_f[i, :f.nlev_f + 1] = f.lev_f[:f.nlev_f + 1]
             lev_b[i, :f.nlev_b + 1] = f.lev_b[:f.nlev_b + 1]
-        if max(rows) > 25000:
-            raise ValueError("1D block too large for the single-CTA ILU sweep (shared memory)")
         perms = [getattr(f, "perm", None) for f in factors]
         T = lambda a, dt=torch.int32: torch.as_tensor(np.ascontiguousarray(a).ravel(), dtype=dt, device=device)  # noqa: E731
         self._t = dict(row_start=T(row_start), ptr=T(ptr), col=T(col), val=T(val, torch.float64), diag=T(diag),
@@ -779,7 +777,13 @@ def ilu0_apply(fact: IluFactorization, r):
 
 
 class IluPreconditioner(Preconditioner):
+    """ILU(0) preconditioner (krylov.py:279-283): host factor, device sweeps (x in shared
+    memory for small factors, in global memory for the 3D baseline on C)."""
+
     def __init__(self, A):
+        if hasattr(A, "prob") and hasattr(A, "matvec"):  # this package's device reduced_operator
+            from .assembly import host_reduced_operator
+            A = host_reduced_operator(A.prob.systems[0])
         self.fact = ilu0(A)
 
     def apply(self, r):

@@ -417,8 +417,25 @@ def gen_gmg():
     dump("gmg", **out)
 
 
+def gen_ilu3d():
+    # the 3D ILU(0) baseline on a reduced operator too large for the shared-memory sweep (33^3)
+    grid = geometry.StructuredGrid(33)
+    g = geometry.generate_graph(geometry.GraphFamilySpec(n_branches=5), 3)
+    s = assembly.assemble_coupled_system(grid, g, assembly.PhysicalParams())
+    C = assembly.reduced_operator(s).tocsr()
+    f = krylov.ilu0(C)
+    rng = np.random.default_rng(41)
+    r = rng.standard_normal(grid.num_nodes)
+    b = rng.standard_normal(grid.num_nodes)
+    x, rep = krylov.fgmres(C, krylov.IluPreconditioner(C), b, restart=30, tol=1e-8, maxit=300)
+    print("ilu3d", rep.iterations, rep.converged)
+    dump("ilu3d_n33", r=r, z=krylov.ilu0_apply(f, r), b=b, iters=np.array(rep.iterations),
+         hist=np.array(rep.residual_history), vertices=g.vertices, edges=g.edges,
+         dirichlet=np.array(g.dirichlet_vertices))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["assembly", "fgmres", "unet", "apply", "cfg1", "direct", "formats", "gmg"]
+    which = sys.argv[1:] or ["assembly", "fgmres", "unet", "apply", "cfg1", "direct", "formats", "gmg", "ilu3d"]
     if "assembly" in which:
         gen_assembly()
     if "fgmres" in which:
@@ -435,3 +452,5 @@ if __name__ == "__main__":
         gen_formats()
     if "gmg" in which:
         gen_gmg()
+    if "ilu3d" in which:
+        gen_ilu3d()

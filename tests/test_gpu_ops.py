@@ -341,3 +341,16 @@ def test_coupled_spmv_129_batched_equals_serial_bitwise(gpu):
         Yi = pb.zeros()
         CoupledOperator(pb).matvec(X, Yi, torch.tensor([i], dtype=torch.int32, device="cuda"))
         assert torch.equal(Yi[i], Y[i])
+
+
+def test_ilu3d_baseline_large_vs_reference(gpu):
+    """3D ILU(0) on C at 33^3 (beyond the shared-memory sweep: x stays in global memory):
+    the apply is bitwise equal to the reference's, the preconditioned solve takes its iterations."""
+    from paper_2505_08491_b200 import assembly as A, geometry as G, krylov
+    g = golden("ilu3d_n33")
+    graph = G.Graph1D(g["vertices"], g["edges"], 1e-3, tuple(int(d) for d in g["dirichlet"]))
+    s = A.assemble_coupled_system(G.StructuredGrid(33), graph, A.PhysicalParams())
+    P = krylov.IluPreconditioner(A.reduced_operator(s))
+    assert np.array_equal(P.apply(g["r"]), g["z"])
+    x, rep = krylov.fgmres(A.reduced_operator(s), P, g["b"], restart=30, tol=1e-8, maxit=300)
+    assert rep.converged and abs(rep.iterations - int(g["iters"])) <= 1
