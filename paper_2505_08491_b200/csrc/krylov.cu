@@ -28,10 +28,20 @@ enum OrthMode { DOT = 0, UPD_DOT = 1, UPD_NORM = 2, NORM = 3 };
 #define ORTH_ELEMS 256  // elements per reduction block before the ORTH_CAP x SMs cap (256 vs 512: -2.5% cfg2 solve)
 #endif
 
+// Reduction partition: blocks of a power-of-two chunk (>= ORTH_ELEMS elements)
+// chosen from the power-of-two band of n, so a longer zero-padded tail (a batch
+// whose 1D parts are longer) only adds trailing blocks with zero partials: the
+// summation order of a system's real entries does not depend on the batch.
+inline int64_t red_chunk(int64_t n) {
+  int64_t c = ORTH_ELEMS;
+  const int64_t cap = (int64_t)ORTH_CAP * sm_count();
+  while ((n + c - 1) / c > cap) c *= 2;
+  return c;
+}
+
 inline int red_blocks(int64_t n) {
-  int nb = ceil_div(n, ORTH_ELEMS);
-  int cap = ORTH_CAP * sm_count();
-  return nb < 1 ? 1 : (nb > cap ? cap : nb);
+  const int64_t nb = (n + red_chunk(n) - 1) / red_chunk(n);
+  return nb < 1 ? 1 : (int)nb;
 }
 
 // Deterministic grid reduction without a second launch: every block
@@ -144,7 +154,7 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
                                                          int64_t ldw, int64_t n,
                                                          const double* __restrict__ coef, int cstride,
                                                          double* __restrict__ partial, int pstride,
-                                                         unsigned int* ticket, RedOut R) {
+                                                         unsigned int* ticket, RedOut R, int64_t chunk) {
   MDP_PDL_ENTER();
   constexpr int NACC = (MODE == DOT || MODE == UPD_DOT) ? (NV > 0 ? NV : 1) : 1;
   __shared__ double csh[NV > 0 ? NV : 1];
@@ -153,7 +163,7 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
   const int nv = nvs ? nvs[i] : 0;
-  const int64_t chunk = ((n + gridDim.x - 1) / gridDim.x + 1) & ~(int64_t)1;  // even: 16-byte aligned pairs
+  // chunk: red_chunk(n), a power of two >= 256 (even: 16-byte aligned pairs)
   const int64_t e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
   const double* Vs = V ? V + s * ldv_sys : nullptr;
   double* ws = w + s * ldw;
@@ -305,7 +315,7 @@ static void launch_orth(int nv_max, dim3 grid, cudaStream_t st, const int32_t* s
                         unsigned int* ticket, const RedOut& R) {
 #define MDP_ORTH(NVT)                                                                            \
   ::mdp::launch_k(orth_pass_kernel<NVT, MODE>, grid, 128, 0, st, sel, V, ldv_sys, ldv_vec, nvs, w, ldw, n, \
-                                                    coef, cstride, partial, pstride, ticket, R)
+                                                    coef, cstride, partial, pstride, ticket, R, red_chunk(n))
   if (MODE == NORM) {
     MDP_ORTH(0);
   } else if (nv_max <= 4) {
@@ -362,13 +372,12 @@ __global__ void basis_update_kernel(const int32_t* sel, double* x, int64_t ldx,
 __global__ void __launch_bounds__(128) residual_kernel(const int32_t* sel, const double* __restrict__ b,
                                                         const double* __restrict__ y, double* r,
                                                         int64_t ld, int64_t n, double* partial,
-                                                        unsigned int* ticket, RedOut R) {
+                                                        unsigned int* ticket, RedOut R, int64_t chunk) {
   MDP_PDL_ENTER();
   __shared__ double sh[32];
   __shared__ double mine[1];
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
-  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const int64_t e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
   double acc = 0.0;
   for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
@@ -770,7 +779,7 @@ extern "C" int mdp_norms(int32_t nsel, const int32_t* sel, const double* x, int6
   R.ostride = 1;
   R.mode = 1;
   ::mdp::launch_k(orth_pass_kernel<0, NORM>, dim3(nb, nsel), 128, 0, st, sel, nullptr, 0, 0, nullptr, const_cast<double*>(x),
-                                                            ldx, n, nullptr, 0, W.partial, 1, W.ticket, R);
+                                                            ldx, n, nullptr, 0, W.partial, 1, W.ticket, R, red_chunk(n));
   MDP_LAUNCH_CHECK("mdp_norms");
   return MDP_OK;
 }
@@ -806,7 +815,8 @@ extern "C" int mdp_residual(int32_t nsel, const int32_t* sel, const double* b, c
   R.ostride = 1;
   R.nk = 1;
   R.mode = 1;
-  ::mdp::launch_k(residual_kernel, dim3(nb, nsel), 128, 0, st, sel, b, y, r, ld, n, W.partial, W.ticket, R);
+  ::mdp::launch_k(residual_kernel, dim3(nb, nsel), 128, 0, st, sel, b, y, r, ld, n, W.partial, W.ticket, R,
+                  red_chunk(n));
   MDP_LAUNCH_CHECK("mdp_residual");
   return MDP_OK;
 }

@@ -279,3 +279,60 @@ def test_speculative_step_batched_cycle_ends(gpu, speculative):
         reps = solver.solve()
         out.append([(reps[i].iterations, reps[i].breakdowns, list(reps[i].residual_history)) for i in range(3)])
     assert out[0] == out[1]
+
+
+def test_batched_solve_with_zero_rhs_system(gpu):
+    """A zero right-hand side inside a batch: that system returns (0 iterations, converged,
+    history [0.0], x = 0) as krylov.py:111-114 does, and the others are unaffected."""
+    import torch
+    from paper_2505_08491_b200 import assembly as A, geometry as G, harness, neural
+    grid = G.StructuredGrid(17)
+    systems = [A.assemble_coupled_system(grid, G.random_tree(4 + 2 * i, 60 + i, 0.02),
+                                         A.PhysicalParams(epsilon=0.02, beta=1.0), elems_per_edge=8)
+               for i in range(3)]
+    st = harness.CoupledStrategy(tol=1e-8, maxit=20, restart=10, inner_iterations=3,
+                                 three_d={"type": "neural", "params": neural.perturbed_params(2),
+                                          "smoothing": {"maxit": 2}})
+    solver = harness.CoupledSolver(systems, st)
+    F = solver.F.clone()
+    F[1].zero_()
+    reps = solver.solve(F)
+    assert reps[1].iterations == 0 and reps[1].converged and reps[1].residual_history == [0.0]
+    assert float(solver.outer.x[1].abs().max()) == 0.0
+    solo = harness.CoupledSolver([systems[0]], st).solve()[0]
+    assert reps[0].iterations == solo.iterations and reps[0].residual_history == solo.residual_history
+
+
+def test_empty_selection_calls_are_noops(gpu):
+    """nsel = 0 through the C ABI does nothing and reports success."""
+    import torch
+    from paper_2505_08491_b200 import _ext, assembly as A, geometry as G
+    from paper_2505_08491_b200.operators import CoupledOperator, ReducedOperator
+    s = A.assemble_coupled_system(G.StructuredGrid(9), G.random_tree(3, 4, 1e-3), A.PhysicalParams(epsilon=1e-3),
+                                  elems_per_edge=2)
+    pb = A.DeviceProblem([s])
+    X, Y = pb.zeros().normal_(), pb.zeros()
+    empty = torch.zeros(0, dtype=torch.int32, device="cuda")
+    CoupledOperator(pb).matvec(X, Y, empty)
+    ReducedOperator(pb).matvec(X, Y, empty)
+    ReducedOperator(pb).jacobi(X, X, Y, 0.5, pb.zeros(), empty)
+    torch.cuda.synchronize()
+    assert float(Y.abs().max()) == 0.0
+
+
+def test_batched_solve_equals_serial_unequal_1d_sizes(gpu, tmp_path):
+    """Batched == serial bitwise also when the systems' 1D parts differ in length
+    (the outer Krylov vectors are zero-padded to the batch's longest 1D part)."""
+    from paper_2505_08491_b200 import assembly as A, geometry as G, harness
+    grid = G.StructuredGrid(17)
+    systems = [A.assemble_coupled_system(grid, G.random_tree(3 + 3 * i, 70 + i, 0.02),
+                                         A.PhysicalParams(epsilon=0.02, beta=1.0), elems_per_edge=6 + 4 * i)
+               for i in range(3)]
+    assert len({s.n1 for s in systems}) == 3
+    spec = {"type": "neural", "params": _params(tmp_path, 2), "smoothing": {"maxit": 2}}
+    st = harness.CoupledStrategy(tol=1e-8, maxit=25, restart=10, inner_iterations=3, three_d=spec)
+    batched = harness.solve_coupled(systems, st)
+    for s, (u3b, u1b, rb) in zip(systems, batched):
+        u3, u1, r = harness.solve_coupled(s, st)
+        assert r.iterations == rb.iterations and r.residual_history == rb.residual_history
+        assert np.array_equal(u3, u3b) and np.array_equal(u1, u1b)
