@@ -785,9 +785,17 @@ class IluPreconditioner(Preconditioner):
             from .assembly import host_reduced_operator
             A = host_reduced_operator(A.prob.systems[0])
         self.fact = ilu0(A)
+        self._dev = None
 
     def apply(self, r):
         return ilu0_apply(self.fact, r)
+
+    def apply_device(self, V, Z, sel, idx=None):
+        """Z_s = ILU(V_s) for the listed systems of (nsys, ld) storages (one factor shared)."""
+        if self._dev is None:
+            self._dev = DeviceIlu([self.fact])
+        for s in (sel.cpu().tolist() if idx is None else idx):
+            self._dev.apply(V[s:s + 1], Z[s:s + 1], V.shape[1], nsys=1)
 
 
 # ---------------------------------------------------------------------------

@@ -131,3 +131,51 @@ class CouplingOps:
         cnt, sp = sel_args(sel, self.prob.nsys)
         _ext.check(self.lib.mdp_stencil_apply(self.prob.desc, cnt, sp, X.data_ptr(), self.prob.ld,
                                               Y.data_ptr(), self.prob.ld, _ext.stream()))
+
+
+class _CsrProblem:
+    """Single-system storage descriptor for CsrOperator (what FgmresEngine needs)."""
+
+    def __init__(self, n: int, device):
+        self.n, self.nsys, self.device = n, 1, device
+        self.ld = (n + 31) // 32 * 32
+
+    def zeros(self):
+        import torch
+        return torch.zeros((1, self.ld), dtype=torch.float64, device=self.device)
+
+
+class CsrOperator:
+    """A general sparse matrix (e.g. the 1D block A11) as a device operator,
+    y = A x one row per thread in CSR order (``mdp_csr_spmv``, csrc/gmg.cu),
+    so ``krylov.fgmres`` can solve with it (training.generate_rhs)."""
+
+    def __init__(self, A, device="cuda"):
+        import scipy.sparse as sp
+        import torch
+        A = sp.csr_matrix(A)
+        if A.shape[0] != A.shape[1]:
+            raise ValueError("CsrOperator needs a square matrix")
+        self.shape = A.shape
+        self.host = A
+        self.ptr = torch.as_tensor(A.indptr.astype(np.int32), device=device)
+        self.col = torch.as_tensor(A.indices.astype(np.int32), device=device)
+        self.val = torch.as_tensor(A.data.astype(np.float64), device=device)
+        self.prob = _CsrProblem(A.shape[0], device)
+        self.lib = _ext.lib()
+
+    def matvec(self, X, Y, sel=None):
+        if sel is not None and int(sel.numel()) == 0:
+            return
+        _ext.check(self.lib.mdp_csr_spmv(self.shape[0], self.ptr.data_ptr(), self.col.data_ptr(),
+                                         self.val.data_ptr(), X.data_ptr(), Y.data_ptr(), 0, _ext.stream()))
+
+    def __matmul__(self, x):
+        import torch
+        x = np.asarray(x, dtype=float)
+        if x.shape != (self.shape[0],):
+            raise ValueError(f"dimension mismatch: {self.shape} @ {x.shape}")
+        X, Y = self.prob.zeros(), self.prob.zeros()
+        X[0, :self.shape[0]] = torch.as_tensor(x, device=self.prob.device)
+        self.matvec(X, Y)
+        return Y[0, :self.shape[0]].cpu().numpy()

@@ -434,8 +434,39 @@ def gen_ilu3d():
          dirichlet=np.array(g.dirichlet_vertices))
 
 
+def gen_training():
+    # dataset build + FP64 training (training.py:124-287) on the reference tests' small dataset
+    # (tests/test_training.py:31-40): 5 family graphs at n = 9, random augmentation
+    grid, params = geometry.StructuredGrid(9), assembly.PhysicalParams()
+    graphs = [geometry.generate_graph(geometry.GraphFamilySpec(n_branches=3 + 4 * i), 50 + i) for i in range(5)]
+    ds = training.build_dataset(grid, graphs, params, training.AugmentationSpec("random", 4), val_fraction=0.2, seed=0)
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        for i, g in enumerate(graphs):
+            geometry.save_graph(g, Path(td) / "g.json")
+            out[f"graph{i}"] = np.frombuffer((Path(td) / "g.json").read_bytes(), dtype=np.uint8).copy()
+    out["samples"] = np.stack([np.stack([s.vector for s in r.samples]) for r in ds.records])
+    out["tags"] = np.array([[s.tag for s in r.samples] for r in ds.records])
+    out["train_indices"], out["val_indices"] = np.array(ds.train_indices), np.array(ds.val_indices)
+    alpha = training.compute_alpha(ds)
+    out["alpha"] = np.array(alpha)
+    out["risk_init1"] = np.array(training.risk(neural.init_unet_params(1), ds, ds.train_samples(), alpha))
+    s0 = assembly.assemble_coupled_system(grid, graphs[0], params)
+    b0 = training.generate_rhs(s0)
+    out["rhs0"] = b0
+    out["krylov0"] = np.stack(training.augment_krylov(assembly.reduced_operator(s0), b0, 4, 5))
+    p, hist = training.train(ds, training.TrainConfig(epochs=2, seed=0))
+    out["history"] = np.array(hist)
+    for key, arr in p.arrays():
+        out[f"sum:{key}"] = np.array([arr.sum(), (arr * arr).sum()])
+    for key in ("head2.kernel", "head2.bias", "head1.bias", "enc1a.bias", "dec1.bias"):
+        out[f"p:{key}"] = dict(p.arrays())[key]
+    print("training history", hist)
+    dump("training_n9", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["assembly", "fgmres", "unet", "apply", "cfg1", "direct", "formats", "gmg", "ilu3d"]
+    which = sys.argv[1:] or ["assembly", "fgmres", "unet", "apply", "cfg1", "direct", "formats", "gmg", "ilu3d", "training"]
     if "assembly" in which:
         gen_assembly()
     if "fgmres" in which:
@@ -454,3 +485,5 @@ if __name__ == "__main__":
         gen_gmg()
     if "ilu3d" in which:
         gen_ilu3d()
+    if "training" in which:
+        gen_training()
