@@ -21,8 +21,8 @@ import numpy as np
 from . import _ext
 from .assembly import CoupledSystem, DeviceProblem, full_rhs, host_reduced_operator, one_d_operator
 from .geometry import DistanceField, distance_field_device
-from .krylov import (DeviceIlu, FgmresEngine, FixedStepFgmres, GmgPreconditioner, IluPreconditioner, SolveReport,
-                     direct_1d, gmg_build, ilu0)
+from .krylov import (DeviceIlu, ExactPreconditioner, FgmresEngine, FixedStepFgmres, GmgPreconditioner,
+                     IluPreconditioner, SolveReport, direct_1d, gmg_build, ilu0)
 from .neural import PATH_TCGEN05, UNetParams, device_net, load_checkpoint
 from .operators import CoupledOperator, CouplingOps, ReducedOperator
 from .training import BatchedNeural, NeuralPreconditioner
@@ -30,9 +30,11 @@ from .training import BatchedNeural, NeuralPreconditioner
 
 @dataclass
 class CoupledStrategy:
-    """harness.py:324-339.  ``one_d``: 'ilu0' (the reference default) or 'direct'
-    (exact 1D solve, harness.py:356-358); 'schur' (a dense Schur complement
-    built from N1 sparse-direct 3D solves) is not on the device path."""
+    """harness.py:324-339.  ``one_d``: 'ilu0' (the reference default), 'direct'
+    (exact 1D solve, harness.py:356-358) or 'schur' (the true Schur complement,
+    harness.py:359-368); ``three_d``: a preconditioner spec or 'direct' (exact
+    3D solve, harness.py:373-375).  The exact variants factor dense matrices in
+    HBM (krylov.ExactPreconditioner), so they are limited to small grids."""
 
     tol: float = 1e-15
     maxit: int = 2000
@@ -47,8 +49,8 @@ def build_preconditioner(spec: dict, grid, C, dfield: DistanceField):
 
     Supported: 'none', 'neural' (checkpoint path or in-memory ``params``,
     optional ``smoothing``/``zero_distance``), the 'gmg' baseline (device
-    V-cycles) and 'ilu0' (host factor, device level-scheduled sweeps).  'exact'
-    is outside the device path.
+    V-cycles), 'ilu0' (host factor, device level-scheduled sweeps) and 'exact'
+    (dense device Cholesky, small grids).
     """
     kind = spec.get("type", "none")
     if kind == "none":
@@ -61,6 +63,8 @@ def build_preconditioner(spec: dict, grid, C, dfield: DistanceField):
                                     zero_distance=spec.get("zero_distance", False))
     if kind == "ilu0" and C is not None:
         return IluPreconditioner(C)
+    if kind == "exact" and C is not None:
+        return ExactPreconditioner(C)
     if kind == "gmg":  # the multigrid baseline (harness.py:218-221)
         levels = spec.get("levels", _default_levels(grid.n))
         return GmgPreconditioner(gmg_build(grid, C, levels), cycles=spec.get("cycles", 10))
@@ -74,6 +78,20 @@ def _default_levels(n: int) -> int:
         n = (n - 1) // 2 + 1
         levels += 1
     return levels
+
+
+class _BatchedExact:
+    """Per-system exact (dense Cholesky) solves behind the batched apply_device interface."""
+
+    def __init__(self, factors):
+        self.factors = factors
+
+    def first_sweep_spec(self):
+        return None
+
+    def apply_device(self, V, Z, sel, idx=None):
+        for s in (sel.cpu().tolist() if idx is None else idx):
+            self.factors[s].apply_device(V[s:s + 1], Z[s:s + 1], None, [0])
 
 
 class _BatchedGmg:
@@ -103,8 +121,8 @@ class CoupledSolver:
 
     def __init__(self, systems, strategy: CoupledStrategy, path: int = PATH_TCGEN05, graphs: bool = True):
         import torch
-        if strategy.one_d not in ("ilu0", "direct"):
-            raise ValueError(f"one_d={strategy.one_d!r}: the device path implements 'ilu0' and 'direct'")
+        if strategy.one_d not in ("ilu0", "direct", "schur"):
+            raise ValueError(f"unknown one_d={strategy.one_d!r}: 'ilu0', 'direct' or 'schur'")
         self.systems = list(systems)
         self.st = strategy
         self.prob = DeviceProblem(self.systems)
@@ -115,10 +133,18 @@ class CoupledSolver:
         fac = direct_1d if strategy.one_d == "direct" else ilu0
         self.ilu = DeviceIlu([fac(one_d_operator(s)) for s in self.systems])
         self.lib = _ext.lib()
-        spec = strategy.three_d or {"type": "none"}
+        self.exact3 = None   # three_d == "direct": per-system exact C solves replace the inner FGMRES
+        self.schur = None    # one_d == "schur": per-system LU of the dense Schur complement
+        if strategy.three_d == "direct" or strategy.one_d == "schur":
+            self.exact3 = [ExactPreconditioner(host_reduced_operator(s)) for s in self.systems]
+        if strategy.one_d == "schur":
+            self.schur = [self._schur_lu(s, f) for s, f in zip(self.systems, self.exact3)]
+        spec = {"type": "none"} if strategy.three_d == "direct" else (strategy.three_d or {"type": "none"})
         kind = spec.get("type", "none")
         self.inner = None
-        if kind == "neural":
+        if kind == "exact":
+            self.inner = _BatchedExact([ExactPreconditioner(host_reduced_operator(s)) for s in self.systems])
+        elif kind == "neural":
             params = spec.get("params")
             if params is None:
                 params = load_checkpoint(spec["checkpoint"])
@@ -139,21 +165,46 @@ class CoupledSolver:
         self.outer = FgmresEngine(p.nsys, p.n3 + p.n1max, p.ld, strategy.restart)
         self.inner_eng = FgmresEngine(p.nsys, p.n3, p.ld, strategy.inner_iterations)
         self.fixed = FixedStepFgmres(p.nsys, p.n3, p.ld, strategy.inner_iterations)
-        self.graphs = graphs
+        self.direct3 = strategy.three_d == "direct"
+        if strategy.three_d != "direct":
+            self.exact3 = None
+        # the dense-factor solves (cuSOLVER via torch) run eagerly, outside CUDA graphs
+        self.graphs = graphs and self.schur is None and not self.direct3 and kind != "exact"
         self.b3 = p.zeros()
         self.F = p.pack([full_rhs(s) for s in self.systems])
 
+    @staticmethod
+    def _schur_lu(s, exact):
+        """LU of S = A11 - (w M10) C^-1 (w M01), C^-1 by the dense device factor (harness.py:359-368)."""
+        import torch
+        w = s.params.coupling_weight
+        dev = exact.L.device
+        W01 = torch.as_tensor((w * s.M01).toarray(), device=dev)
+        S = torch.as_tensor(one_d_operator(s).toarray(), device=dev) - \
+            torch.as_tensor((w * s.M10).toarray(), device=dev) @ exact.solve_device(W01)
+        return torch.linalg.lu_factor(S)
+
     def _block_precond(self, V, Z, sel, idx):
+        import torch
         p = self.prob
         m = int(sel.numel())
         n3 = p.n3
-        # z1 = ILU(r1)   (krylov.py:270-276 via harness.py:390)
-        _ext.check(self.lib.mdp_ilu0_apply(self.ilu.desc, m, sel.data_ptr(), V.data_ptr() + 8 * n3,
-                                           Z.data_ptr() + 8 * n3, p.ld, _ext.stream()))
+        if self.schur is not None:  # z1 = S^-1 r1 (harness.py:368)
+            for s in idx:
+                n1 = self.systems[s].n1
+                LU, piv = self.schur[s]
+                Z[s, n3:n3 + n1] = torch.linalg.lu_solve(LU, piv, V[s, n3:n3 + n1, None])[:, 0]
+        else:  # z1 = ILU(r1)   (krylov.py:270-276 via harness.py:390)
+            _ext.check(self.lib.mdp_ilu0_apply(self.ilu.desc, m, sel.data_ptr(), V.data_ptr() + 8 * n3,
+                                               Z.data_ptr() + 8 * n3, p.ld, _ext.stream()))
         # r0 - w M01 z1  (harness.py:391)
         _ext.check(self.lib.mdp_copy_vec(m, sel.data_ptr(), V.data_ptr(), p.ld, self.b3.data_ptr(), p.ld, None, 0,
                                          n3, _ext.stream()))
         self.cpl.minus_w_m01(Z, self.b3, sel)
+        if self.direct3:  # z0 = C^-1 (r0 - w M01 z1)  (harness.py:373-375)
+            for s in idx:
+                Z[s, :n3] = self.exact3[s].solve_device(self.b3[s, :n3])
+            return
         # z0 = 3-step inner FGMRES on C (harness.py:385-387)
         m_in = self.st.inner_iterations
         P = self.inner.apply_device if self.inner is not None else None

@@ -56,6 +56,57 @@ class Preconditioner:
         return self.apply(r)
 
 
+# Dense device factorizations behind the exact baselines are limited to this many
+# bytes per matrix (n = 33: C is 35937^2 doubles = 10.3 GB; 65^3 would need 600 GB).
+EXACT_MAX_BYTES = 48 << 30
+
+
+class ExactPreconditioner(Preconditioner):
+    """Direct solve, the reference's 'perfect' preconditioner (krylov.py:54-61), on
+    the device: C is symmetric positive definite (Neumann with a reaction term, or
+    symmetric Dirichlet elimination), so it is factored once as a dense Cholesky
+    product in HBM (cuSOLVER through torch.linalg) and every apply is two
+    triangular solves.  Grids whose dense matrix exceeds EXACT_MAX_BYTES raise."""
+
+    def __init__(self, A, device="cuda"):
+        import torch
+        if hasattr(A, "prob") and hasattr(A, "matvec"):
+            from .assembly import host_reduced_operator
+            A = host_reduced_operator(A.prob.systems[0])
+        A = sp.coo_matrix(A)
+        n = A.shape[0]
+        if A.shape[0] != A.shape[1]:
+            raise ValueError("exact solve needs a square matrix")
+        if n * n * 8 > EXACT_MAX_BYTES:
+            raise ValueError(f"dense exact solve of a {n}x{n} matrix exceeds {EXACT_MAX_BYTES >> 30} GiB")
+        D = torch.zeros((n, n), dtype=torch.float64, device=device)
+        D.index_put_((torch.as_tensor(A.row, device=device), torch.as_tensor(A.col, device=device)),
+                     torch.as_tensor(A.data, device=device), accumulate=True)
+        self.L, info = torch.linalg.cholesky_ex(D)
+        del D
+        if int(info) != 0:
+            raise ValueError("exact solve: matrix is not positive definite")
+        self.n = n
+
+    def solve_device(self, B):
+        """X = A^-1 B for a device (n,) or (n, k) tensor."""
+        import torch
+        vec = B.dim() == 1
+        X = torch.cholesky_solve(B[:, None] if vec else B, self.L)
+        return X[:, 0] if vec else X
+
+    def apply(self, r):
+        import torch
+        r = np.asarray(r, dtype=float)
+        if r.shape != (self.n,):
+            raise ValueError("right-hand side length mismatch")
+        return self.solve_device(torch.as_tensor(r, device=self.L.device)).cpu().numpy()
+
+    def apply_device(self, V, Z, sel, idx=None):
+        for s in (sel.cpu().tolist() if idx is None else idx):
+            Z[s, :self.n] = self.solve_device(V[s, :self.n])
+
+
 def spmv(A, x):
     """CSR / device-operator product with a dimension check (krylov.py:64-69)."""
     x = np.asarray(x)

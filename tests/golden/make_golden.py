@@ -465,8 +465,53 @@ def gen_training():
     dump("training_n9", **out)
 
 
+def gen_exact():
+    # exact baselines: ExactPreconditioner (krylov.py:54-61), three_d="direct" and one_d="schur"
+    # (harness.py:356-375) on the reference tests' single-segment system (tests/test_harness.py:26-30,
+    # 176-187, 207-219) and the n = 9 family system
+    import scipy.sparse.linalg as spla
+    grid = geometry.StructuredGrid(9)
+    out = {}
+
+    def seg(eps):
+        g = geometry.Graph1D(np.array([[0.31, 0.42, 0.11], [0.58, 0.63, 0.87]]), np.array([[0, 1]]), eps, (0,))
+        return assembly.assemble_coupled_system(grid, g, assembly.PhysicalParams(epsilon=eps))
+
+    s = seg(1e-3)
+    C = assembly.reduced_operator(s)
+    w = s.params.coupling_weight
+    lu_c0 = spla.splu(C.tocsc())
+    coupling = np.column_stack([lu_c0.solve(col) for col in (w * s.M01).toarray().T])
+    out["seg_schur"] = assembly.one_d_operator(s).toarray() - (w * s.M10).toarray() @ coupling
+    for label, one_d in (("schur", "schur"), ("direct", "direct")):
+        st = harness.CoupledStrategy(tol=1e-12, maxit=50, one_d=one_d, three_d="direct")
+        u3, u1, rep = harness.solve_coupled(s, st)
+        out[f"seg_{label}_iters"] = np.array(rep.iterations)
+        out[f"seg_{label}_hist"] = np.array(rep.residual_history)
+        out[f"seg_{label}_u3"], out[f"seg_{label}_u1"] = u3, u1
+        print("exact seg", label, rep.iterations, rep.rel_residual)
+    for eps in (1e-6, 1e-9):
+        u3, _, rep = harness.solve_coupled(seg(eps), harness.CoupledStrategy(tol=1e-12, maxit=50, one_d="direct",
+                                                                              three_d="direct"))
+        out[f"vanish_{eps:g}_norm"] = np.array(np.linalg.norm(u3))
+        out[f"vanish_{eps:g}_iters"] = np.array(rep.iterations)
+    g = geometry.generate_graph(geometry.GraphFamilySpec(n_branches=5), 3)
+    f = assembly.assemble_coupled_system(grid, g, assembly.PhysicalParams())
+    Cf = assembly.reduced_operator(f)
+    r = np.random.default_rng(5).standard_normal((2, f.n3))
+    out["fam_r"], out["fam_z"] = r, np.array([krylov.ExactPreconditioner(Cf).apply(v) for v in r])
+    st = harness.CoupledStrategy(tol=1e-8, maxit=60, restart=30, inner_iterations=3, one_d="ilu0",
+                                 three_d={"type": "exact"})
+    u3, u1, rep = harness.solve_coupled(f, st)
+    out["fam_inner_exact_iters"] = np.array(rep.iterations)
+    out["fam_inner_exact_hist"] = np.array(rep.residual_history)
+    out["fam_inner_exact_u3"], out["fam_inner_exact_u1"] = u3, u1
+    print("exact fam inner", rep.iterations, rep.rel_residual)
+    dump("exact_n9", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["assembly", "fgmres", "unet", "apply", "cfg1", "direct", "formats", "gmg", "ilu3d", "training"]
+    which = sys.argv[1:] or ["assembly", "fgmres", "unet", "apply", "cfg1", "direct", "formats", "gmg", "ilu3d", "training", "exact"]
     if "assembly" in which:
         gen_assembly()
     if "fgmres" in which:
@@ -487,3 +532,5 @@ if __name__ == "__main__":
         gen_ilu3d()
     if "training" in which:
         gen_training()
+    if "exact" in which:
+        gen_exact()

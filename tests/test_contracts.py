@@ -53,7 +53,7 @@ def test_apply_contracts():
 
 def test_coupled_strategy_contracts():
     s = _system()
-    with pytest.raises(ValueError):  # 'schur' is not on the device path
-        harness.solve_coupled(s, harness.CoupledStrategy(one_d="schur"))
+    with pytest.raises(ValueError):  # unknown 1D block treatment
+        harness.solve_coupled(s, harness.CoupledStrategy(one_d="bogus"))
     with pytest.raises(ValueError):
         harness.build_preconditioner({"type": "exact"}, s.grid, None, None)
