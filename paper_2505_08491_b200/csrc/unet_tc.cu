@@ -263,8 +263,11 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  // prologue (barriers, TMEM, tensor-map prefetch) overlapped with the previous grid
-  MDP_PDL_ENTER();
+  // prologue (barriers, TMEM, tensor-map prefetch) overlapped with the previous grid; the
+  // weights are never written on the device, so their producer (warp 0) streams the first
+  // stages without waiting for it either
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (warp != 0) asm volatile("griddepcontrol.wait;" ::: "memory");
   const int nunits = A.fold ? 9 : 27;
 
   if (warp == 3) {
