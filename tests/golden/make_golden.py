@@ -455,6 +455,9 @@ def gen_training():
     b0 = training.generate_rhs(s0)
     out["rhs0"] = b0
     out["krylov0"] = np.stack(training.augment_krylov(assembly.reduced_operator(s0), b0, 4, 5))
+    dk = training.build_dataset(grid, graphs[:2], params, training.AugmentationSpec("krylov", 3, 2), val_fraction=0.5,
+                                seed=4)
+    out["krylov_samples"] = np.stack([np.stack([s.vector for s in r.samples]) for r in dk.records])
     p, hist = training.train(ds, training.TrainConfig(epochs=2, seed=0))
     out["history"] = np.array(hist)
     for key, arr in p.arrays():

@@ -91,3 +91,17 @@ def test_dataset_directory_round_trip(gpu, ds, tmp_path):
         assert np.array_equal(a.dfield.values, b.dfield.values)
         assert all(np.array_equal(x.vector, y.vector) and x.tag == y.tag for x, y in zip(a.samples, b.samples))
     assert T.compute_alpha(back) == T.compute_alpha(dset)
+
+
+def test_krylov_augmented_dataset(gpu, ds):
+    """AugmentationSpec("krylov", 3, 2): Arnoldi vectors q_2..q_4 of span(b, Cb, ...) on the device
+    (training.py:139-160) against the reference's dataset."""
+    from paper_2505_08491_b200 import assembly as A, geometry as G, training as T
+    _, graphs = ds
+    g = golden("training_n9")
+    dk = T.build_dataset(G.StructuredGrid(9), graphs[:2], A.PhysicalParams(), T.AugmentationSpec("krylov", 3, 2),
+                         val_fraction=0.5, seed=4)
+    for i, rec in enumerate(dk.records):
+        assert [s.tag for s in rec.samples] == ["physics", "krylov", "krylov", "krylov"]
+        for v, ref in zip([s.vector for s in rec.samples], g["krylov_samples"][i]):
+            assert rel(v, ref) <= 1e-8
