@@ -560,11 +560,10 @@ class FixedStepFgmres:
         self.nsys, self.n, self.ld, self.k = nsys, n, ld, m
         f = dict(dtype=torch.float64, device=device)
         self.V = torch.zeros((nsys, m + 1, ld), **f)
-        self.Z = torch.zeros((nsys, m, ld), **f)
+        self.Z = torch.zeros((m, nsys, ld), **f)  # slot-major: P writes Z[j] (an (nsys, ld) storage) in place
         self.x = torch.zeros((nsys, ld), **f)
         self.w = torch.zeros((nsys, ld), **f)
         self.vcur = torch.zeros((nsys, ld), **f)
-        self.zcur = torch.zeros((nsys, ld), **f)
         self.hcol = torch.zeros((nsys, m + 2), **f)
         self.H = torch.zeros((nsys, m + 1, m), **f)
         self.cs = torch.zeros((nsys, m), **f)
@@ -597,22 +596,21 @@ class FixedStepFgmres:
                                      self.vcur.data_ptr(), ld, n, self.H.data_ptr(), self.cs.data_ptr(),
                                      self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), jo, om, dg, st))
         for j in range(k):
+            Zj = self.Z[j]
             if P is None:
-                _ext.check(L.mdp_copy_vec(m, sp_, self.vcur.data_ptr(), ld, self.zcur.data_ptr(), ld, None, 0, n, st))
+                _ext.check(L.mdp_copy_vec(m, sp_, self.vcur.data_ptr(), ld, Zj.data_ptr(), ld, None, 0, n, st))
             elif pre is not None:
-                P(self.vcur, self.zcur, sel, idx, presmoothed=True)
+                P(self.vcur, Zj, sel, idx, presmoothed=True)
             else:
-                P(self.vcur, self.zcur, sel, idx)
-            Zj = self.Z[:, j, :]
-            _ext.check(L.mdp_copy_vec(m, sp_, self.zcur.data_ptr(), ld, Zj.data_ptr(), k * ld, None, 0, n, st))
-            A(self.zcur, self.w, sel)
+                P(self.vcur, Zj, sel, idx)
+            A(Zj, self.w, sel)
             _ext.check(L.mdp_arnoldi_givens(m, sp_, self.V.data_ptr(), (k + 1) * ld, ld, self.nvs[j].data_ptr(), k,
                                             self.w.data_ptr(), ld, n, self.hcol.data_ptr(), self.vcur.data_ptr(), ld,
                                             self.work.data_ptr(), j, self.H.data_ptr(), self.cs.data_ptr(),
                                             self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(),
                                             jo if j + 1 < k else None, om, dg, st))
         x = self.x if out is None else out
-        _ext.check(L.mdp_fixed_finish(m, sp_, k, k, self.Z.data_ptr(), k * ld, ld, x.data_ptr(), ld, n,
+        _ext.check(L.mdp_fixed_finish(m, sp_, k, k, self.Z.data_ptr(), ld, self.nsys * ld, x.data_ptr(), ld, n,
                                       self.H.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(), st))
 
 
