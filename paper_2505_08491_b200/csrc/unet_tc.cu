@@ -507,26 +507,47 @@ __global__ void conv_split_reduce_kernel(const float4* __restrict__ part, int ks
   const int So = pool ? S / 2 : S;
   const int64_t S3 = (int64_t)S * S * S, So3 = (int64_t)So * So * So;
   const int64_t total = (int64_t)nb * cq * So3;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = t % So3;
-    const int64_t bq = t / So3;
+  const int64_t kstride = (int64_t)nb * cq * S3;
+  // pool: 8 lanes per output quad, one 2x2x2 window voxel each (the split-K sums
+  // run in parallel; the max over the window is exact in any order); the loop
+  // trip count is warp-uniform so the shuffles see all 32 lanes
+  const int wlog = pool ? 3 : 0;
+  const int lane = threadIdx.x & 31;
+  const int64_t items = total << wlog;
+  for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x - lane); t0 < items;
+       t0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = t0 + lane;
+    const bool live = t < items;
+    const int64_t o = live ? t >> wlog : 0;
+    const int d = pool ? (int)(t & 7) : 0;
+    const int64_t v = o % So3;
+    const int64_t bq = o / So3;
     const int q = bq % cq, b = bq / cq;
     const int x = v % So, y = (v / So) % So, z = v / ((int64_t)So * So);
+    const int xx = pool ? 2 * x + (d & 1) : x, yy = pool ? 2 * y + ((d >> 1) & 1) : y, zz = pool ? 2 * z + (d >> 2) : z;
+    const int64_t vi = ((int64_t)zz * S + yy) * S + xx;
+    const float4* pp = part + ((int64_t)b * cq + q) * S3 + vi;
+    float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) {
+      m = pp[0];
+#pragma unroll 4
+      for (int k = 1; k < ksplit; ++k) {
+        const float4 p = pp[k * kstride];
+        m.x += p.x; m.y += p.y; m.z += p.z; m.w += p.w;
+      }
+    }
+    if (pool) {
+#pragma unroll
+      for (int off = 1; off < 8; off <<= 1) {
+        m.x = fmaxf(m.x, __shfl_xor_sync(0xffffffffu, m.x, off));
+        m.y = fmaxf(m.y, __shfl_xor_sync(0xffffffffu, m.y, off));
+        m.z = fmaxf(m.z, __shfl_xor_sync(0xffffffffu, m.z, off));
+        m.w = fmaxf(m.w, __shfl_xor_sync(0xffffffffu, m.w, off));
+      }
+    }
+    if (!live || d != 0) continue;
     const float4 bb = bias ? make_float4(bias[4 * q], bias[4 * q + 1], bias[4 * q + 2], bias[4 * q + 3])
                            : make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 m = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-    const int nw = pool ? 8 : 1;
-    for (int d = 0; d < nw; ++d) {
-      const int xx = pool ? 2 * x + (d & 1) : x, yy = pool ? 2 * y + ((d >> 1) & 1) : y,
-                zz = pool ? 2 * z + (d >> 2) : z;
-      const int64_t vi = ((int64_t)zz * S + yy) * S + xx;
-      float4 acc = part[((int64_t)b * cq + q) * S3 + vi];
-      for (int k = 1; k < ksplit; ++k) {
-        const float4 p = part[(((int64_t)k * nb + b) * cq + q) * S3 + vi];
-        acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
-      }
-      m.x = fmaxf(m.x, acc.x); m.y = fmaxf(m.y, acc.y); m.z = fmaxf(m.z, acc.z); m.w = fmaxf(m.w, acc.w);
-    }
     m.x += bb.x; m.y += bb.y; m.z += bb.z; m.w += bb.w;
     if (relu) m = make_float4(fmaxf(m.x, 0.f), fmaxf(m.y, 0.f), fmaxf(m.z, 0.f), fmaxf(m.w, 0.f));
     out[((int64_t)b * out_cq + out_q0 + q) * So3 + v] = tf32_round4(m);
@@ -906,7 +927,7 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   } else if (A.ksplit > 1) {
     const int pool = epi == EPI_POOL;
     const int So = pool ? S / 2 : S;
-    const int64_t total = (int64_t)nb * (cout / 4) * So * So * So;
+    const int64_t total = (int64_t)nb * (cout / 4) * So * So * So * (pool ? 8 : 1);
     int bx = ceil_div(total, 256);
     bx = bx > 4 * sm_count() ? 4 * sm_count() : bx;
     ::mdp::launch_k(conv_split_reduce_kernel, bx, 256, 0, st, A.partial, A.ksplit, nb, cout / 4, S, bias, relu, pool, out,
