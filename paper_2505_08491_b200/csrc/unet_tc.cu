@@ -928,9 +928,9 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
     const int pool = epi == EPI_POOL;
     const int So = pool ? S / 2 : S;
     const int64_t total = (int64_t)nb * (cout / 4) * So * So * So * (pool ? 8 : 1);
-    int bx = ceil_div(total, 256);
-    bx = bx > 4 * sm_count() ? 4 * sm_count() : bx;
-    ::mdp::launch_k(conv_split_reduce_kernel, bx, 256, 0, st, A.partial, A.ksplit, nb, cout / 4, S, bias, relu, pool, out,
+    int bx = ceil_div(total, 128);  // 128-thread blocks: small layers spread over more SMs
+    bx = bx > 8 * sm_count() ? 8 * sm_count() : bx;
+    ::mdp::launch_k(conv_split_reduce_kernel, bx, 128, 0, st, A.partial, A.ksplit, nb, cout / 4, S, bias, relu, pool, out,
                                                  out_cq, out_q0);
     MDP_LAUNCH_CHECK("conv_split_reduce_kernel");
   }
