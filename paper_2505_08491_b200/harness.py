@@ -94,6 +94,24 @@ class _BatchedExact:
             self.factors[s].apply_device(V[s:s + 1], Z[s:s + 1], None, [0])
 
 
+class _BatchedIlu:
+    """Per-system 3D ILU(0) of C (krylov.py:247-284) behind the batched apply_device
+    interface: host factors, one batched device sweep launch (graph-safe)."""
+
+    def __init__(self, systems, ld):
+        self.dev = DeviceIlu([ilu0(host_reduced_operator(s)) for s in systems])
+        self.ld = ld
+        self.lib = _ext.lib()
+
+    def first_sweep_spec(self):
+        return None
+
+    def apply_device(self, V, Z, sel, idx=None, presmoothed=False):
+        # the global-memory sweep keeps x in Z, so V and Z must be distinct storages
+        _ext.check(self.lib.mdp_ilu0_apply(self.dev.desc, int(sel.numel()), sel.data_ptr(), V.data_ptr(),
+                                           Z.data_ptr(), self.ld, _ext.stream()))
+
+
 class _BatchedGmg:
     """Per-system GMG preconditioners behind the batched apply_device interface."""
 
@@ -156,6 +174,8 @@ class CoupledSolver:
             self.inner = BatchedNeural(device_net(params, spec.get("path", path)), dists, p.n, p.ld, p.nsys,
                                        C=self.C, smoothing=smooth,
                                        zero_distance=spec.get("zero_distance", False))
+        elif kind == "ilu0":  # the 3D ILU(0) baseline: one factor of C per system
+            self.inner = _BatchedIlu(self.systems, p.ld)
         elif kind == "gmg":  # the multigrid baseline: one Galerkin hierarchy per system
             levels = spec.get("levels", _default_levels(p.n))
             self.inner = _BatchedGmg([GmgPreconditioner(gmg_build(s.grid, host_reduced_operator(s), levels),
@@ -169,7 +189,10 @@ class CoupledSolver:
         if strategy.three_d != "direct":
             self.exact3 = None
         # the dense-factor solves (cuSOLVER via torch) run eagerly, outside CUDA graphs
-        self.graphs = graphs and self.schur is None and not self.direct3 and kind != "exact"
+        # the fixed-step device solve keeps y in a 64-entry shared array (mdp_fixed_finish):
+        # longer inner solves take the host-driven FgmresEngine path
+        self.graphs = graphs and self.schur is None and not self.direct3 and kind != "exact" \
+            and strategy.inner_iterations <= 64
         self.b3 = p.zeros()
         self.F = p.pack([full_rhs(s) for s in self.systems])
 

@@ -617,21 +617,53 @@ class FixedStepFgmres:
 # ---------------------------------------------------------------------------
 # drop-in host-vector entry point
 
-def _host_apply(op):
-    if sp.issparse(op):
-        return lambda v: op @ v
-    if callable(op):
+class _HostCallableOperator:
+    """A host callable ``v -> A v`` behind the device-operator interface (one
+    host round trip per product), so ``fgmres`` accepts any callable as the
+    reference does (krylov.py:72-75)."""
+
+    def __init__(self, fn, n: int, device="cuda"):
+        from .operators import _CsrProblem
+        self.fn, self.shape = fn, (n, n)
+        self.prob = _CsrProblem(n, device)
+
+    def matvec(self, X, Y, sel=None):
+        import torch
+        if sel is not None and int(sel.numel()) == 0:
+            return
+        n = self.shape[0]
+        y = np.asarray(self.fn(X[0, :n].cpu().numpy()), dtype=float)
+        if y.shape != (n,):
+            raise ValueError(f"operator returned shape {y.shape}, expected ({n},)")
+        Y[0, :n] = torch.as_tensor(y, device=Y.device)
+
+
+def _device_operator(op, n: int):
+    """The operator argument of ``fgmres`` as a device operator (krylov.py:72-75):
+    this package's device operators pass through, sparse / dense matrices are
+    uploaded as a device CSR operator (``operators.CsrOperator``), any other
+    callable is applied on the host."""
+    from .operators import CsrOperator
+    if hasattr(op, "matvec") and hasattr(op, "prob"):
         return op
+    if sp.issparse(op) or isinstance(op, np.ndarray):
+        if op.shape[1] != n:
+            raise ValueError(f"dimension mismatch: {op.shape} @ ({n},)")
+        return CsrOperator(sp.csr_matrix(op))
+    if callable(op):
+        return _HostCallableOperator(op, n)
     raise TypeError("operator must be a sparse matrix, a device operator or a callable")
 
 
 def fgmres(apply_A, precond, b, restart: int = 20, tol: float = 1e-6, maxit: int = 1000, x0=None):
     """Drop-in ``krylov.fgmres`` (krylov.py:88-182) on the device.
 
-    ``apply_A`` must be a device operator (``full_operator`` /
-    ``reduced_operator`` of this package); ``precond`` is None, a device
-    preconditioner of this package, or any callable / Preconditioner on
-    host vectors (then applied through a host round trip).  Returns
+    ``apply_A`` is a device operator of this package (``full_operator`` /
+    ``reduced_operator``), a scipy sparse or dense matrix (uploaded as a
+    device CSR operator) or any host callable (applied through a host round
+    trip), as in the reference (krylov.py:72-75); ``precond`` is None, a
+    device preconditioner of this package, or any callable / Preconditioner
+    on host vectors (then applied through a host round trip).  Returns
     ``(x, SolveReport)`` with host numpy x.
     """
     import torch
@@ -641,11 +673,10 @@ def fgmres(apply_A, precond, b, restart: int = 20, tol: float = 1e-6, maxit: int
         raise ValueError("tol must be positive")
     if precond is not None and not (isinstance(precond, Preconditioner) or callable(precond)):
         raise TypeError("preconditioner must be None, callable, or Preconditioner")
-    if not hasattr(apply_A, "matvec"):
-        raise TypeError("apply_A must be a device operator (full_operator / reduced_operator)")
-    prob = apply_A.prob
     b = np.asarray(b, dtype=float)
     n = b.shape[0]
+    apply_A = _device_operator(apply_A, n)
+    prob = apply_A.prob
     if n != apply_A.shape[0]:
         raise ValueError(f"dimension mismatch: {apply_A.shape} @ {b.shape}")
     eng = FgmresEngine(1, n, prob.ld, restart)
@@ -906,6 +937,10 @@ class GmgHierarchy:
     device: object = None   # _GmgDevice
 
 
+# largest coarsest level the device V-cycle inverts densely (17^3 = 4913 unknowns: 190 MB)
+GMG_MAX_COARSE = 4913
+
+
 class _GmgDevice:
     def __init__(self, hier: GmgHierarchy):
         import torch
@@ -915,6 +950,7 @@ class _GmgDevice:
         self.P = [_DevCsr(P) for P in hier.prolongs]
         self.PT = [_DevCsr(P.T.tocsr()) for P in hier.prolongs]
         # the coarsest solve (splu in the reference) as a dense inverse: the level has 27-125 unknowns
+        # with the default level count (gmg_build rejects coarsest levels above GMG_MAX_COARSE)
         Mc = hier.matrices[-1].toarray()
         self.Minv = torch.as_tensor(np.linalg.inv(Mc).ravel(), device="cuda")
         f = dict(dtype=torch.float64, device="cuda")
@@ -1007,6 +1043,12 @@ def gmg_build(grid, fine_operator, levels: int) -> GmgHierarchy:
         prolongs.append(P)
         sizes.append(nc)
         n = nc
+    # the device V-cycle inverts the coarsest level densely: a hierarchy that stops
+    # coarsening early is rejected rather than densified (levels=1 at 33^3 would be
+    # a 35937^2 inverse)
+    if mats[-1].shape[0] > GMG_MAX_COARSE:
+        raise ValueError(f"coarsest GMG level has {mats[-1].shape[0]} unknowns (> {GMG_MAX_COARSE}); "
+                         f"use more levels so the dense coarse solve stays small")
     import scipy.sparse.linalg as spla
     coarse_lu = spla.splu(sp.csc_matrix(mats[-1]))
     hier = GmgHierarchy(mats, prolongs, coarse_lu, sizes)

@@ -108,3 +108,57 @@ def test_weight_packing_layouts():
     assert pt[1, 10, 5, 3] == t[10, 16 + 3].ravel()[5]
     p0 = neural.pack_tconv(t, neural.PATH_TCGEN05).reshape(8, 16, 32, 4)  # [tap][quad][cout][4]
     assert abs(p0[5, 3, 17, 2] - t[3 * 4 + 2, 17].ravel()[5]) <= 1e-3 * abs(t[14, 17].ravel()[5])
+
+
+_CTYPE = {"int32_t": "c_int", "int64_t": "c_long", "double": "c_double", "float": "c_float", "size_t": "c_ulong"}
+
+
+def header_struct(name):
+    """(field, ctype-name) pairs of ``typedef struct name {...}`` in the header."""
+    text = (ROOT / "include" / "mdp_b200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    body = re.search(rf"typedef struct {name}\s*\{{(.*?)\}}\s*{name}\s*;", text, flags=re.S).group(1)
+    out = []
+    for decl in body.split(";"):
+        decl = " ".join(decl.split())
+        if not decl:
+            continue
+        m = re.match(r"(const )?(\w+)(\*?) (.*)", decl)
+        _, base, ptr, names = m.groups()
+        for nm in names.split(","):
+            nm = nm.strip()
+            arr = re.match(r"(\*?)(\w+)\[(\d+)\]", nm)
+            star = ptr or nm.startswith("*")
+            nm = nm.lstrip("*")
+            if arr:
+                out.append((arr.group(2), "ptr", int(arr.group(3))))
+            else:
+                out.append((nm, "ptr" if star else _CTYPE[base], 1))
+    return out
+
+
+def _binding_fields(struct):
+    import ctypes as C
+    out = []
+    for nm, ty in struct._fields_:
+        if issubclass(ty, C.Array):
+            out.append((nm, "ptr" if ty._type_ is C.c_void_p else ty._type_.__name__, ty._length_))
+        else:
+            out.append((nm, "ptr" if ty is C.c_void_p else ty.__name__, 1))
+    return out
+
+
+@pytest.mark.parametrize("cname,pyname", [("mdp_problem", "MdpProblem"), ("mdp_ilu", "MdpIlu"),
+                                          ("mdp_unet", "MdpUnet")])
+def test_struct_layout_header_vs_binding(cname, pyname):
+    """Every descriptor struct of the header and its ctypes mirror agree field by field
+    (a shorter ctypes struct would make the C side read past its end)."""
+    assert header_struct(cname) == _binding_fields(getattr(_ext, pyname))
+
+
+def test_integration_doc_struct_matches_binding():
+    """The MdpProblem snippet in INTEGRATION.md is the full struct, not an abridged prefix."""
+    text = (ROOT / "INTEGRATION.md").read_text()
+    snippet = re.search(r"class MdpProblem\(C\.Structure\):.*?_fields_ = \[(.*?)\]\n", text, flags=re.S).group(1)
+    names = re.findall(r'\("(\w+)"', snippet)
+    assert names == [nm for nm, _ in _ext.MdpProblem._fields_]

@@ -57,3 +57,11 @@ def test_coupled_strategy_contracts():
         harness.solve_coupled(s, harness.CoupledStrategy(one_d="bogus"))
     with pytest.raises(ValueError):
         harness.build_preconditioner({"type": "exact"}, s.grid, None, None)
+
+
+def test_gmg_rejects_large_dense_coarse_level():
+    """A hierarchy that stops coarsening early would need a dense inverse of the
+    fine grid; it is rejected before any factorisation or device upload."""
+    s = _system(n=33, eps=1e-3)
+    with pytest.raises(ValueError, match="coarsest GMG level"):
+        krylov.gmg_build(s.grid, A.host_reduced_operator(s), 1)

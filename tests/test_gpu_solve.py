@@ -26,19 +26,19 @@ def _params(tmp_path, seed=0):
     return neural.load_checkpoint(path)
 
 
-@pytest.mark.parametrize("label", ["none", "neural_s"])
+@pytest.mark.parametrize("label", ["none", "ilu0", "neural_s"])
 def test_solve_coupled_n9_vs_reference(gpu, label, tmp_path):
     from paper_2505_08491_b200 import harness
     g = golden("apply_solve_n9")
     s = _n9()
-    spec = {"type": "none"}
+    spec = {"type": label}
     if label == "neural_s":
         spec = {"type": "neural", "params": _params(tmp_path), "smoothing": {"maxit": 2}}
     st = harness.CoupledStrategy(tol=1e-6, maxit=120, restart=30, inner_iterations=3, three_d=spec)
     u3, u1, rep = harness.solve_coupled(s, st)
     want = int(g[f"solve_{label}_iters"])
     assert rep.converged == bool(g[f"solve_{label}_conv"])
-    if label == "none":
+    if label in ("none", "ilu0"):
         assert rep.iterations == want
     else:
         assert abs(rep.iterations - want) <= 2
@@ -175,8 +175,19 @@ def test_fgmres_dropin_with_device_operator(gpu, tmp_path):
     P = training.NeuralPreconditioner(_params(tmp_path), d)
     _, rep2 = krylov.fgmres(C, P, b, tol=1e-4, maxit=400)
     assert rep2.iterations > 0 and len(rep2.residual_history) >= 2
+    # the operator may also be a scipy sparse matrix or any host callable (krylov.py:72-75)
+    Ch = A.host_reduced_operator(s)
+    xs, rs = krylov.fgmres(Ch, None, b, restart=20, tol=1e-8, maxit=500)
+    xc, rc = krylov.fgmres(lambda v: Ch @ v, None, b, restart=20, tol=1e-8, maxit=500)
+    for xx, rr in ((xs, rs), (xc, rc)):
+        assert rr.converged and abs(rr.iterations - ro.iterations) <= 2
+        assert np.linalg.norm(xx - xo) <= 1e-6 * np.linalg.norm(xo)
+    with pytest.raises(ValueError):
+        krylov.fgmres(Ch[:, :-1], None, b)
     with pytest.raises(TypeError):
         krylov.fgmres(C, 3.0, b)
+    with pytest.raises(TypeError):
+        krylov.fgmres(3.0, None, b)
     with pytest.raises(ValueError):
         krylov.fgmres(C, None, b, restart=0)
 
@@ -216,7 +227,7 @@ def test_direct_1d_batched_random_trees(gpu):
         assert np.linalg.norm(Z[i, :len(r)].cpu().numpy() - want) <= 1e-12 * np.linalg.norm(want)
 
 
-@pytest.mark.parametrize("label", ["none"])  # the 3D ilu0 inner preconditioner is not on the device path
+@pytest.mark.parametrize("label", ["none", "ilu0"])
 def test_solve_coupled_direct_1d_vs_reference(gpu, label):
     from paper_2505_08491_b200 import harness
     g = golden("direct_n9")
