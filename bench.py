@@ -1,6 +1,6 @@
 """Benchmark of the neural-preconditioned coupled FGMRES solve on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg4]
 
 A step is one full coupled solve (outer FGMRES(restart) with the ILU(0) 1D
 block and the 3-step inner FGMRES on C preconditioned by the Jacobi(2,2/3)-
@@ -32,9 +32,9 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "preconditioned FGMRES solves/sec + applies/sec at 1 B200; % HBM/tensor roofline"
-# outer iterations of the full solve, from the parity-checked GPU run (the
-# reference arm times a bounded sample of iterations and extrapolates)
-EXPECTED_ITERS = {"cfg1": None, "cfg2": None, "cfg3": None, "cfg4": None}
+# the e2e leg (drop-in API from host buffers) repeats the solve; at cfg4 a solve is
+# ~15 s, so it is timed over at most this many steps
+E2E_MAX_STEPS = 5
 
 
 def peaks():
@@ -199,7 +199,7 @@ def conv_layer_times(n, reps=20):
     return out
 
 
-def target_128(tf32_peak, hbm_peak):
+def target_128(tf32_peak, hbm_peak, layers=None):
     """The north star's target configuration (BASELINE cfg4, 128^3 cells = 129^3
     nodes): conv layers vs the TF32 tensor peak, the CNN forward, and the
     coupled SpMV (L2 flushed before every rep) vs the HBM peak."""
@@ -208,7 +208,7 @@ def target_128(tf32_peak, hbm_peak):
     from paper_2505_08491_b200.operators import CoupledOperator
     from paper_2505_08491_b200.assembly import DeviceProblem
     n = 129
-    layers = conv_layer_times(n, reps=5)
+    layers = layers or conv_layer_times(n, reps=5)
     dom = max(layers, key=lambda k: layers[k]["ms"])
     stack_ms = sum(v["ms"] for v in layers.values())
     stack_fl = sum(v["flops"] for v in layers.values())
@@ -293,50 +293,138 @@ def ncu_traffic(key):
         return None
 
 
-def spmv_roofline(solver, reps=50):
-    """Coupled SpMV: algorithmic bytes 16 (N3 + N1) + 40 Q per system."""
+def spmv_roofline(solver, reps=20):
+    """Coupled SpMV: algorithmic bytes 16 (N3 + N1) + 40 Q per system,
+    L2 flushed (write, then read back) before every rep."""
     import torch
     p = solver.prob
     X = p.zeros().normal_()
     Y = p.zeros()
-    ms = device_ms(lambda: solver.A.matvec(X, Y), reps)
+    flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device="cuda")
+    ms = device_ms(lambda: solver.A.matvec(X, Y), reps, flush=flush)
+    del flush
     nbytes = sum(16 * (p.n3 + int(n1)) for n1 in p.n1) + 40 * p.Qtot
     return ms, nbytes
 
 
+def config_dict(name, wl):
+    """The workload description printed identically by both arms."""
+    return {"workload": name, **wl.meta, "systems_per_gpu": len(wl.systems), "restart": wl.restart,
+            "rtol": wl.tol, "maxit": wl.maxit, "inner_iterations": wl.inner_iterations,
+            "smoothing": list(wl.smoothing), "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# z-planes of the CNN slab the operator-model CPU sample runs the oracle forward on
+# (op2 = 0 / op1 = 1 like the full 65^3 / 129^3 grids; cost scales with the voxel count)
+SLAB_Z = 9
+
+
+def oracle_sampler(name, wl):
+    """CPU oracle timing of the workload (test infrastructure as the timed baseline).
+
+    Returns (sample(), describe(times)): ``sample()`` runs one bounded piece
+    of the oracle solve and returns (seconds measured, extrapolated seconds
+    per outer FGMRES iteration of ONE system).
+
+    * cfg1 / cfg2: two outer iterations of the oracle coupled solve
+      (oracle.solve_coupled, the restatement of harness.py:342-398).
+    * cfg3 / cfg4 (65^3 / 129^3: one oracle CNN forward alone takes 4 / 40 s):
+      the per-operator model of one outer iteration: 3
+      smoothed CNN applies (1 forward + 5 C-SpMVs each), 6 more C-SpMVs of
+      the 3-step inner FGMRES, the A-SpMV plus its share of the per-cycle
+      residual SpMVs, and one MGS step over the cycle-average number of basis
+      vectors.  The forward is timed on a 9-plane z-slab of the grid and
+      scaled by the voxel ratio; the SpMVs and the MGS step run at full size.
+    """
+    import numpy as np
+    import oracle
+    from oracle import problem as OP
+    osys = oracle_system(name)
+    params = oracle.noisy_params(wl.cnn_seed)
+    sm = wl.smoothing
+    if name in ("cfg1", "cfg2"):
+        spec = {"type": "neural", "params": params, "smoothing": sm}
+        it = 2
+
+        def sample():
+            st = oracle.CoupledStrategy(tol=wl.tol, maxit=it, restart=wl.restart,
+                                        inner_iterations=wl.inner_iterations, three_d=spec)
+            t0 = time.perf_counter()
+            oracle.solve_coupled(osys, st)
+            dt = time.perf_counter() - t0
+            return dt, dt / it
+
+        return sample, lambda: f"{it} outer iterations of the oracle coupled solve per sample"
+    A = OP.full_operator(osys)
+    C = OP.reduced_operator(osys)
+    n, n3 = osys.grid.n, osys.n3
+    N = A.shape[0]
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal(N)
+    x3 = x[:n3].copy()
+    slab = rng.standard_normal((2, SLAB_Z, n, n))
+    kavg = (wl.restart + 1) // 2
+    V = rng.standard_normal((kavg, N))
+    m = wl.inner_iterations
+    n_c = m * (sm[0] * 2 + 1) + 2 * m   # smoothing SpMVs of m applies + the inner FGMRES SpMVs
+    n_a = 1 + 2.0 / wl.restart
+
+    def sample():
+        t0 = time.perf_counter()
+        oracle.unet_forward(params, slab)
+        t_cnn = (time.perf_counter() - t0) * n / SLAB_Z
+        t1 = time.perf_counter()
+        C @ x3
+        t_c = time.perf_counter() - t1
+        t2 = time.perf_counter()
+        w = A @ x
+        t_a = time.perf_counter() - t2
+        t3 = time.perf_counter()
+        for i in range(kavg):  # krylov.py:138-140
+            h = w @ V[i]
+            w -= h * V[i]
+        np.linalg.norm(w)
+        t_mgs = time.perf_counter() - t3
+        dt = time.perf_counter() - t0
+        return dt, m * t_cnn + n_c * t_c + n_a * t_a + t_mgs
+
+    return sample, lambda: (f"per-operator model of one outer iteration: oracle U-Net forward on a {SLAB_Z}x{n}x{n} "
+                            f"slab scaled by {n}/{SLAB_Z} (x{m} applies), {n_c} C-SpMVs, {n_a:.2f} A-SpMVs, "
+                            f"one MGS step over {kavg} vectors, all at {n}^3")
+
+
 def run_reference(args):
     """CPU arm: the oracle restatement of the reference path on the host cores."""
-    import oracle
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2505_08491_b200 import configs
     wl = configs.CONFIGS[args.workload]()
-    osys = oracle_system(args.workload)
-    spec = {"type": "neural", "params": oracle.noisy_params(wl.cnn_seed), "smoothing": wl.smoothing}
-    sample = args.ref_iters
-    times = []
+    if args.maxit:
+        wl.maxit = args.maxit
+    sample, describe = oracle_sampler(args.workload, wl)
+    times, per_iter = [], []
     for step in range(args.warmup + args.steps):
-        st = oracle.CoupledStrategy(tol=wl.tol, maxit=sample, restart=wl.restart,
-                                    inner_iterations=wl.inner_iterations, three_d=spec)
-        t0 = time.perf_counter()
-        oracle.solve_coupled(osys, st)
-        dt = time.perf_counter() - t0
+        dt, pit = sample()
         if step >= args.warmup:
             times.append(dt)
-    per_iter = statistics.median(times) / sample
-    full = args.maxit or EXPECTED_ITERS.get(args.workload) or wl.maxit
-    value = 1.0 / (per_iter * full) * len(wl.systems)
+            per_iter.append(pit)
+    pit = statistics.median(per_iter)
+    full = wl.maxit
+    value = len(wl.systems) / (pit * full * len(wl.systems))
     cores = len(os.sched_getaffinity(0))
+    desc = f"{describe()}; extrapolated to {full} outer iterations per system"
     line = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": statistics.median(times) * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE graphs)",
-            "config": {"workload": args.workload, **wl.meta}, "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port",
-                             "sample": f"{sample} outer iterations of the oracle coupled solve per step, "
-                                       f"extrapolated to {full} iterations (x{len(wl.systems)} systems)"},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": config_dict(args.workload, wl), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port", "sample": desc,
+                             "s_per_outer_iteration": pit},
             "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+DATA = "synthetic (seeded BASELINE graphs, perturbed random-init CNN)"
 
 
 def oracle_system(name):
@@ -350,6 +438,16 @@ def oracle_system(name):
         g = OP.random_tree(8, 1, 0.015)
         return OP.assemble_coupled_system(OP.StructuredGrid(33), g, OP.PhysicalParams(epsilon=0.015, beta=1.0),
                                           n_circle=8, elems_per_edge=16, bc3d="dirichlet", f1d=1.0)
+    if name == "cfg3":
+        import numpy as np
+        beta = float(np.random.default_rng(2).uniform(0.5, 2.0, 16)[0])
+        return OP.assemble_coupled_system(OP.StructuredGrid(65), OP.random_tree(32, 2000, 0.01),
+                                          OP.PhysicalParams(epsilon=0.01, beta=beta), n_circle=8,
+                                          elems_per_edge=16, bc3d="dirichlet", f1d=1.0)
+    if name == "cfg4":
+        return OP.assemble_coupled_system(OP.StructuredGrid(129), OP.random_tree(64, 3, 0.008),
+                                          OP.PhysicalParams(epsilon=0.008, beta=1.0), n_circle=8,
+                                          elems_per_edge=32, bc3d="dirichlet", f1d=1.0, check_radius=False)
     raise ValueError(f"no oracle builder for {name}")
 
 
@@ -426,8 +524,9 @@ def run_ours(args):
 
     # -- e2e through the drop-in API with host buffers, on every rank (replicas), whole-job
     #    solves/s = all ranks' solves / the slowest rank's wall time
-    e2e_ms, h2d, d2h = e2e_steps(wl, strat, args.steps)
-    e2e_value, _, _ = aggregate_throughput(e2e_ms * args.steps, len(wl.systems) * args.steps, device="cuda")
+    e2e_n = min(args.steps, E2E_MAX_STEPS)
+    e2e_ms, h2d, d2h = e2e_steps(wl, strat, e2e_n)
+    e2e_value, _, _ = aggregate_throughput(e2e_ms * e2e_n, len(wl.systems) * e2e_n, device="cuda")
 
     out = None
     if rank == 0:
@@ -437,39 +536,39 @@ def run_ours(args):
         layers = conv_layer_times(n)
         per_fwd = {k: v["ms"] for k, v in layers.items()}
         dom = max(per_fwd, key=per_fwd.get)
-        tf32 = measure_tf32_peak()
+        # tensor denominator: kind::tf32 runs at half the dense bf16 rate; the measured bf16
+        # burst peak (the layer is timed alone) / 2.  cuBLAS TF32 is reported beside it.
+        tf32 = pk["bf16_tflops"] / 2
+        cublas_tf32 = measure_tf32_peak()
         L = layers[dom]
         spmv_ms, spmv_bytes = spmv_roofline(solver)
         line = {
             "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64 system / tf32 CNN",
-            "data": "synthetic (seeded BASELINE graphs, perturbed random-init CNN)",
-            "config": {"workload": args.workload, **wl.meta, "systems_per_gpu": len(wl.systems),
-                       "restart": wl.restart, "rtol": wl.tol, "maxit": wl.maxit,
-                       "inner_iterations": wl.inner_iterations, "smoothing": list(wl.smoothing),
-                       "l2": "flushed between timed steps (256 MiB write)"},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 system / tf32 CNN", "data": DATA,
+            "config": config_dict(args.workload, wl),
             "iterations": iters, "converged": conv, "rel_residual": rel,
             "applies_per_s": applies_per_s,
             "roofline": {"bound": "tensor", "kernel": f"conv3_tc_kernel ({dom}, S={L['S']})",
                          "achieved": L["tflops"], "peak": tf32, "unit": "TFLOP/s",
                          "frac": L["tflops"] / tf32,
                          "traffic": (ncu_traffic(f"conv3_tc_kernel {dom} S={L['S']}") or {}).get("dram_bytes"),
-                         "peak_note": "cuBLAS TF32 8192^3 measured in this run",
-                         "frac_of_bf16_measured_over_2": L["tflops"] / (pk["bf16_tflops"] / 2)},
+                         "peak_note": f"MEASURED_PEAKS bf16_tflops/2 ({pk['source']}); cuBLAS TF32 8192^3 "
+                                      f"in this run: {cublas_tf32:.1f} TF/s",
+                         "frac_of_cublas_tf32": L["tflops"] / cublas_tf32},
             "conv_layers": layers,
             "roofline_spmv": {"bound": "hbm", "kernel": "coupled SpMV (stencil+Pi)",
                               "achieved": spmv_bytes / (spmv_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"],
                               "unit": "GB/s", "frac": spmv_bytes / (spmv_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
                               "frac_of_8tbs_spec": spmv_bytes / (spmv_ms * 1e-3) / 8e12,
-                              "note": "L2-resident at this size" if spmv_bytes < 2 * 126e6 else ""},
+                              "note": "one system; L2 flushed (write, then read back) before every rep"},
             "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": h2d * world,
-                    "d2h_bytes_per_step": d2h * world},
+                    "d2h_bytes_per_step": d2h * world, "steps": e2e_n},
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
         }
         if not args.no_target:
-            line["target_128"] = target_128(tf32, pk["hbm_gbs"])
+            line["target_128"] = target_128(tf32, pk["hbm_gbs"], layers if n == 129 else None)
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.workload, wl, iters)
         out = line
@@ -500,23 +599,17 @@ def e2e_steps(wl, strat, steps):
     return ms, h2d, d2h
 
 
-def cpu_baseline(name, wl, gpu_iters, sample_iters=3):
-    import oracle
-    try:
-        osys = oracle_system(name)
-    except ValueError:
-        return {"value": None, "unit": "solves/s", "cores": len(os.sched_getaffinity(0)), "kind": "port",
-                "sample": "no oracle builder for this workload"}
-    spec = {"type": "neural", "params": oracle.noisy_params(wl.cnn_seed), "smoothing": wl.smoothing}
-    st = oracle.CoupledStrategy(tol=wl.tol, maxit=sample_iters, restart=wl.restart,
-                                inner_iterations=wl.inner_iterations, three_d=spec)
-    t0 = time.perf_counter()
-    oracle.solve_coupled(osys, st)
-    dt = time.perf_counter() - t0
+def cpu_baseline(name, wl, gpu_iters, samples=3):
+    """The oracle on the host cores, a bounded sample of the same workload (see oracle_sampler)."""
+    sample, describe = oracle_sampler(name, wl)
+    sample()  # warm (numba-free numpy, but first-touch allocations)
+    res = [sample() for _ in range(samples)]
+    pit = statistics.median(r[1] for r in res)
     full = max(gpu_iters)
-    return {"value": 1.0 / (dt / sample_iters * full), "unit": "solves/s", "cores": len(os.sched_getaffinity(0)),
-            "kind": "port", "sample": f"{sample_iters} outer iterations of the oracle coupled solve "
-                                      f"({dt:.1f} s), extrapolated to the {full} iterations of the full solve"}
+    return {"value": 1.0 / (pit * full), "unit": "solves/s", "cores": len(os.sched_getaffinity(0)),
+            "kind": "port", "s_per_outer_iteration": pit,
+            "sample": f"{describe()}; {samples} samples ({sum(r[0] for r in res):.1f} s), extrapolated to the "
+                      f"{full} outer iterations per system of the GPU solve"}
 
 
 def main():
@@ -525,9 +618,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
     ap.add_argument("--maxit", type=int, default=0)
-    ap.add_argument("--ref-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-target", action="store_true", help="skip the 128^3 target-config rooflines")
     args = ap.parse_args()

@@ -149,3 +149,21 @@ def test_gmg_hierarchy_contracts():
         krylov.gmg_build(grid, Kl, 0)
     with pytest.raises(ValueError):
         krylov.GmgPreconditioner(None, cycles=0)
+
+
+def test_cfg4_geometry_index_sets_vs_reference():
+    """The north-star 128^3 geometry (64-segment seed-3 tree, 32 elements per segment,
+    8-point ring average) under the reference's own assemble_coupled_system
+    (R = 0.0078 < h, golden cfg4_ref): Pi / Psi / W, A11 and M10 bit-exact."""
+    g = golden("cfg4_ref")
+    s = A.assemble_coupled_system(G.StructuredGrid(129), G.random_tree(64, 3, 0.0078),
+                                  A.PhysicalParams(epsilon=0.0078, beta=1.0), n_circle=8, elems_per_edge=32)
+    assert s.n1 == int(g["n1"])
+    r = s.restriction
+    same_csr(r.matrix, g, "T")
+    same_csr(r.basis_1d, g, "psi")
+    assert np.array_equal(r.weights, g["W"])
+    same_csr(A.one_d_operator(s), g, "A11")
+    same_csr(s.M10, g, "M10")
+    assert np.array_equal(s.rhs1, g["rhs1"])
+    assert np.array_equal(s.rhs0[g["touched"]], g["rhs0_touched"])
