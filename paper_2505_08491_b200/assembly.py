@@ -354,6 +354,16 @@ def diag_reduced(system: CoupledSystem) -> np.ndarray:
     return d
 
 
+def _ranges(starts, counts):
+    """Concatenated index ranges [starts[i], starts[i] + counts[i])."""
+    starts = np.asarray(starts, dtype=np.int64)
+    counts = np.asarray(counts, dtype=np.int64)
+    if counts.sum() == 0:
+        return np.zeros(0, dtype=np.int64)
+    off = np.repeat(starts - np.concatenate([[0], np.cumsum(counts)[:-1]]), counts)
+    return off + np.arange(int(counts.sum()))
+
+
 class DeviceProblem:
     """Batched device descriptor of systems sharing one grid (``mdp_problem``)."""
 
@@ -419,11 +429,11 @@ class DeviceProblem:
             nz = np.nonzero(np.diff(TT.indptr))[0]
             if bmask is not None:
                 nz = nz[~bmask[nz]]
-            for node in nz:
-                a, b = TT.indptr[node], TT.indptr[node + 1]
-                u_q.append(TT.indices[a:b].astype(np.int32) + q0)
-                u_val.append(TT.data[a:b])
-                u_ptr.append(u_ptr[-1] + (b - a))
+            cnt_u = TT.indptr[nz + 1] - TT.indptr[nz]
+            src = _ranges(TT.indptr[nz], cnt_u)
+            u_q.append(TT.indices[src].astype(np.int32) + q0)
+            u_val.append(TT.data[src])
+            u_ptr.extend((u_ptr[-1] + np.cumsum(cnt_u)).tolist())
             u_node.append(nz.astype(np.int32))
             u_start.append(u_start[-1] + len(nz))
             # 1D rows
@@ -494,6 +504,7 @@ class DeviceProblem:
         P.ell_w = ell_w
         if os.environ.get("MDP_NO_ELL"):  # A/B only: the CSR pull
             P.ell_q, P.ell_val = None, None
+
         self.desc = P
         self.s_work = torch.zeros(max(1, self.Qtot), dtype=torch.float64, device=dev)
         self.ilu = None
