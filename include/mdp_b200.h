@@ -166,16 +166,24 @@ int mdp_ilu0_apply(const mdp_ilu* f, int32_t nsel, const int32_t* sel,
 /* ------------------------------------------------------------------ */
 /* Krylov vector kernels (krylov.py:88-182).  V is [nsys][kmax+1][ld].   */
 
-/* Fused Arnoldi orthogonalisation of w against V[0..nv[s]) (CGS2, two
- * classical passes = MGS-equivalent stability), replaces the MGS loop
- * krylov.py:138-141.  Writes hcol[s][0..kmax] = projection coefficients,
+/* Fused Arnoldi orthogonalisation of w against V[0..nv[s]), replaces the MGS
+ * loop krylov.py:138-141.  Writes hcol[s][0..kmax] = projection coefficients,
  * hcol[s][kmax+1] = ||w_final||, and V[s][nv[s]] = w_final/||w_final||
  * (vnext, also copied to vcur when non-NULL).  work: scratch of
- * mdp_arnoldi_work_bytes(). */
+ * mdp_arnoldi_work_bytes().
+ * gram != NULL ([nsys][kmax+1][kmax+1], owned by the caller, indexed by system
+ * id): modified Gram-Schmidt from one pass of dot products.  The reference's
+ * sequential projections h_m = V_m.(w - sum_{c<m} h_c V_c) equal the solution
+ * of the unit lower triangular system (I + L) h = V^T w with L the strictly
+ * lower part of V^T V; row nv of L (the new vector against the old ones) is
+ * produced by the update pass of the same step, so V is read twice per step
+ * (dots; update + Gram row + norm) and the step is three launches.  A cycle
+ * must run its steps nv = 1, 2, ... in order (each step writes row nv).
+ * gram == NULL: CGS2 (two classical passes, three reads of V, four launches). */
 size_t mdp_arnoldi_work_bytes(int32_t nsel, int32_t kmax, int64_t n);
 int mdp_arnoldi(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
                 const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n,
-                double* hcol, double* vcur, int64_t ldc, void* work, void* stream);
+                double* hcol, double* vcur, int64_t ldc, double* gram, void* work, void* stream);
 
 /* out[i] = ||x_s||_2 for the selected systems (two-stage deterministic). */
 int mdp_norms(int32_t nsel, const int32_t* sel, const double* x, int64_t ldx, int64_t n,
@@ -222,7 +230,7 @@ int mdp_fixed_start(int32_t nsel, const int32_t* sel, int32_t k, const double* b
                     double omega, const double* diag, void* stream);
 int mdp_arnoldi_givens(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
                        const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n, double* hcol,
-                       double* vcur, int64_t ldc, void* work, int32_t j, double* H, double* cs, double* sn,
+                       double* vcur, int64_t ldc, double* gram, void* work, int32_t j, double* H, double* cs, double* sn,
                        double* g, double* flag, double* jac_out, double omega, const double* diag,
                        void* stream);
 /* (jac_out != NULL: also jac_out_s = (omega vcur_s) / diag_s, stride ldc -- the first

@@ -63,7 +63,7 @@ _SIGS = {
     "mdp_ilu0_apply": (_i32, [C.POINTER(MdpIlu), _i32, _vp, _vp, _vp, _i64, _vp]),
     "mdp_arnoldi_work_bytes": (C.c_size_t, [_i32, _i32, _i64]),
     "mdp_arnoldi": (_i32, [_i32, _vp, _vp, _i64, _i64, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _i64,
-                           _vp, _vp]),
+                           _vp, _vp, _vp]),
     "mdp_norms": (_i32, [_i32, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "mdp_scale": (_i32, [_i32, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _vp]),
     "mdp_basis_update": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _i32, _i64, _vp]),
@@ -73,7 +73,7 @@ _SIGS = {
     "mdp_fixed_init": (_i32, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mdp_fixed_start": (_i32, [_i32, _vp, _i32, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
                                _vp, _f64, _vp, _vp]),
-    "mdp_arnoldi_givens": (_i32, [_i32, _vp, _vp, _i64, _i64, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _i32,
+    "mdp_arnoldi_givens": (_i32, [_i32, _vp, _vp, _i64, _i64, _vp, _i32, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i32,
                                   _vp, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _vp]),
     "mdp_fixed_finish": (_i32, [_i32, _vp, _i32, _i32, _vp, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "mdp_givens_step": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

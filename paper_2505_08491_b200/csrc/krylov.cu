@@ -10,7 +10,7 @@
 
 namespace mdp {
 
-enum OrthMode { DOT = 0, UPD_DOT = 1, UPD_NORM = 2, NORM = 3 };
+enum OrthMode { DOT = 0, UPD_DOT = 1, UPD_NORM = 2, NORM = 3, DOT_SOLVE = 4, UPD_DOT_NORM = 5 };
 
 // orth-pass tuning (tools/arnoldi_ab.py, profiles/): blocks per SM cap, elements per
 // thread step (2 = 16-byte loads), independent basis loads per batch
@@ -53,17 +53,22 @@ struct RedOut {
   double* out;      // [nsel][ostride]
   int ostride;
   int nk;           // entries to reduce
-  int mode;         // 0 plain, 1 sqrt, 2 arnoldi finalize (out = ||w||^2)
+  int mode;         // 0 plain, 1 sqrt, 2 arnoldi finalize (out = ||w||^2),
+                    // 3 MGS coefficients from the Gram rows, 4 new Gram row + ||w||
   const double* h1; // mode 2: the two projections, [nsel][kmax+1]
   const double* h2;
-  double* hcol;     // mode 2: [nsel][kmax+2] Hessenberg column + ||w||
+  double* hcol;     // modes 2-4: [nsel][kmax+2] Hessenberg column + ||w||
   int kmax;
   const int32_t* nvs;
+  double* gram;     // modes 3, 4: [nsys][kmax+1][kmax+1], row m = V_m . V_c for c < m
+  const int32_t* sel;
 };
 
+template <int NL = 0>
 __device__ __forceinline__ void finish_reduction(const double* __restrict__ partial, int pstride,
                                                  unsigned int* ticket, const RedOut& R, const double* mine) {
   __shared__ bool last;
+  __shared__ double Ls[NL > 0 ? NL * (NL + 1) : 1];  // mode 3: Gram rows, padded row stride
   const int i = blockIdx.y;
   if (threadIdx.x < R.nk) {
     double* dst = const_cast<double*>(partial) + ((int64_t)i * gridDim.x + blockIdx.x) * pstride;
@@ -108,6 +113,46 @@ __device__ __forceinline__ void finish_reduction(const double* __restrict__ part
     for (int k = threadIdx.x; k <= R.kmax; k += blockDim.x)
       R.hcol[i * (R.kmax + 2) + k] = k < nv ? R.h1[i * (R.kmax + 1) + k] + R.h2[i * (R.kmax + 1) + k] : 0.0;
     if (threadIdx.x == 0) R.hcol[i * (R.kmax + 2) + R.kmax + 1] = sqrt(R.out[i * R.ostride]);
+  }
+  if constexpr (NL > 0) {
+    // Modified Gram-Schmidt from ONE pass of dot products (krylov.py:138-140):
+    // the sequential projections h_m = V_m . (w - sum_{c<m} h_c V_c) equal
+    // h_m = a_m - sum_{c<m} (V_m . V_c) h_c with a = V^T w, i.e. the unit lower
+    // triangular system (I + L) h = a over the strictly lower Gram rows L kept
+    // from the previous steps of this cycle.  Column-oriented forward
+    // substitution in one warp (lane l owns entries l and l + 32), fixed order.
+    const int nv = R.nvs[i];
+    const int s = sys_of(R.sel, i);
+    const double* G = R.gram + (int64_t)s * (R.kmax + 1) * (R.kmax + 1);
+    for (int t2 = threadIdx.x; t2 < nv * nv; t2 += blockDim.x) {
+      const int m = t2 / nv, c = t2 - m * nv;
+      if (c < m) Ls[m * (NL + 1) + c] = __ldcg(G + m * (R.kmax + 1) + c);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int l = threadIdx.x;
+      double* a = R.out + i * R.ostride;
+      double x0 = l < nv ? a[l] : 0.0, x1 = (NL > 32 && l + 32 < nv) ? a[l + 32] : 0.0;
+      for (int c = 0; c < nv; ++c) {
+        const double hc = __shfl_sync(0xffffffffu, c < 32 ? x0 : x1, c & 31);
+        if (l > c && l < nv) x0 -= Ls[l * (NL + 1) + c] * hc;
+        if (NL > 32 && l + 32 > c && l + 32 < nv) x1 -= Ls[(l + 32) * (NL + 1) + c] * hc;
+      }
+      if (l < nv) a[l] = x0;
+      if (NL > 32 && l + 32 < nv) a[l + 32] = x1;
+      for (int k = l; k <= R.kmax; k += 32)
+        R.hcol[i * (R.kmax + 2) + k] = k < nv ? (k < 32 ? x0 : x1) : 0.0;
+    }
+  }
+  if (R.mode == 4) {  // out[0..nv) = V^T w', out[nv] = ||w'||^2: Gram row of the new vector w'/||w'||
+    __syncthreads();
+    const int nv = R.nvs[i];
+    const int s = sys_of(R.sel, i);
+    const double hn = sqrt(R.out[i * R.ostride + nv]);
+    double* G = R.gram + (int64_t)s * (R.kmax + 1) * (R.kmax + 1) + (int64_t)nv * (R.kmax + 1);
+    if (nv <= R.kmax && hn > 0.0)
+      for (int k = threadIdx.x; k < nv; k += blockDim.x) G[k] = R.out[i * R.ostride + k] / hn;
+    if (threadIdx.x == 0) R.hcol[i * (R.kmax + 2) + R.kmax + 1] = hn;
   }
   if (threadIdx.x == 0) ticket[i] = 0u;
 }
@@ -156,10 +201,13 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
                                                          double* __restrict__ partial, int pstride,
                                                          unsigned int* ticket, RedOut R, int64_t chunk) {
   MDP_PDL_ENTER();
-  constexpr int NACC = (MODE == DOT || MODE == UPD_DOT) ? (NV > 0 ? NV : 1) : 1;
+  constexpr bool UPD = MODE == UPD_DOT || MODE == UPD_NORM || MODE == UPD_DOT_NORM;
+  constexpr bool DOTS = MODE == DOT || MODE == UPD_DOT || MODE == DOT_SOLVE || MODE == UPD_DOT_NORM;
+  constexpr bool BOTH = MODE == UPD_DOT_NORM;  // dots and ||w||^2 in the same pass
+  constexpr int NACC = DOTS ? (NV > 0 ? NV : 1) : 1;
   __shared__ double csh[NV > 0 ? NV : 1];
-  __shared__ double wsum[4][NACC];
-  __shared__ double mine[NACC];
+  __shared__ double wsum[4][NACC + 1];
+  __shared__ double mine[NACC + 1];
   const int i = blockIdx.y;
   const int s = sys_of(sel, i);
   const int nv = nvs ? nvs[i] : 0;
@@ -167,11 +215,12 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
   const int64_t e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
   const double* Vs = V ? V + s * ldv_sys : nullptr;
   double* ws = w + s * ldw;
-  if (MODE == UPD_DOT || MODE == UPD_NORM) {
+  if (UPD) {
     for (int k = threadIdx.x; k < NV; k += blockDim.x) csh[k] = k < nv ? coef[i * cstride + k] : 0.0;
     __syncthreads();
   }
   double acc[NACC];
+  double accn = 0.0;
 #pragma unroll
   for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
   // Each thread walks element pairs (16-byte loads: longer contiguous runs per
@@ -182,7 +231,7 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
   for (int64_t e = e0 + ORTH_VEC * threadIdx.x; e < e1; e += ORTH_VEC * blockDim.x) {
     if (ORTH_VEC == 2 && e + 1 < e1) {
       double2 w2 = *reinterpret_cast<const double2*>(ws + e);
-      if (MODE == UPD_DOT || MODE == UPD_NORM) {
+      if (UPD) {
 #pragma unroll
         for (int k0 = 0; k0 < NV; k0 += KB) {
           double2 vv[KB];
@@ -199,7 +248,11 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
         }
         *reinterpret_cast<double2*>(ws + e) = w2;
       }
-      if (MODE == DOT || MODE == UPD_DOT) {
+      if (BOTH) {
+        accn += w2.x * w2.x;
+        accn += w2.y * w2.y;
+      }
+      if (DOTS) {
 #pragma unroll
         for (int k0 = 0; k0 < NACC; k0 += KB) {
           double2 vv[KB];
@@ -222,7 +275,7 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
     }
     for (int64_t f = e; f < e + ORTH_VEC && f < e1; ++f) {
       double we = ws[f];
-      if (MODE == UPD_DOT || MODE == UPD_NORM) {
+      if (UPD) {
 #pragma unroll
         for (int k0 = 0; k0 < NV; k0 += KB) {
           double vv[KB];
@@ -234,7 +287,8 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
         }
         ws[f] = we;
       }
-      if (MODE == DOT || MODE == UPD_DOT) {
+      if (BOTH) accn += we * we;
+      if (DOTS) {
 #pragma unroll
         for (int k0 = 0; k0 < NACC; k0 += KB) {
           double vv[KB];
@@ -260,12 +314,18 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
 #pragma unroll
       for (int k = 0; k < NACC; ++k) wsum[wid][k] = acc[k];
   }
+  if constexpr (BOTH) {  // the norm rides behind the nv dot products (slot nv)
+    for (int o = 16; o > 0; o >>= 1) accn += __shfl_xor_sync(0xffffffffu, accn, o);
+    if (lane == 0) wsum[wid][NACC] = accn;
+  }
   __syncthreads();
   for (int k = threadIdx.x; k < nk; k += blockDim.x)
     mine[k] = ((wsum[0][k] + wsum[1][k]) + wsum[2][k]) + wsum[3][k];
+  if (BOTH && threadIdx.x == 0)
+    mine[nk] = ((wsum[0][NACC] + wsum[1][NACC]) + wsum[2][NACC]) + wsum[3][NACC];
   RedOut Rl = R;
-  Rl.nk = nk;
-  finish_reduction(partial, pstride, ticket, Rl, mine);
+  Rl.nk = BOTH ? nk + 1 : nk;
+  finish_reduction<MODE == DOT_SOLVE ? NV : 0>(partial, pstride, ticket, Rl, mine);
 }
 
 // V[s][nv] = w / hn  (and vcur), exact division like krylov.py:165
@@ -701,31 +761,31 @@ extern "C" size_t mdp_arnoldi_work_bytes(int32_t nsel, int32_t kmax, int64_t n) 
 
 static int arnoldi_impl(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
                         const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n, double* hcol,
-                        double* vcur, int64_t ldc, void* work, void* stream, const GivensArgs& GA,
+                        double* vcur, int64_t ldc, double* gram, void* work, void* stream, const GivensArgs& GA,
                         const JacPre& J);
 
 extern "C" int mdp_arnoldi(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys,
                            int64_t ldv_vec, const int32_t* nv, int32_t kmax, double* w, int64_t ldw,
-                           int64_t n, double* hcol, double* vcur, int64_t ldc, void* work,
+                           int64_t n, double* hcol, double* vcur, int64_t ldc, double* gram, void* work,
                            void* stream) {
-  return arnoldi_impl(nsel, sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n, hcol, vcur, ldc, work, stream,
+  return arnoldi_impl(nsel, sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n, hcol, vcur, ldc, gram, work, stream,
                       GivensArgs{0, 0, nullptr, nullptr, nullptr, nullptr, nullptr}, JacPre{nullptr, 0.0, nullptr});
 }
 
 extern "C" int mdp_arnoldi_givens(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
                                   const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n,
-                                  double* hcol, double* vcur, int64_t ldc, void* work, int32_t j, double* H,
-                                  double* cs, double* sn, double* g, double* flag, double* jac_out, double omega,
-                                  const double* diag, void* stream) {
+                                  double* hcol, double* vcur, int64_t ldc, double* gram, void* work, int32_t j,
+                                  double* H, double* cs, double* sn, double* g, double* flag, double* jac_out,
+                                  double omega, const double* diag, void* stream) {
   MDP_REQUIRE(H && cs && sn && g && flag && j >= 0 && j < kmax, "fused Givens step needs the fixed-step state");
   MDP_REQUIRE(!jac_out || (vcur && diag), "the fused first Jacobi sweep needs vcur and diag");
-  return arnoldi_impl(nsel, sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n, hcol, vcur, ldc, work, stream,
+  return arnoldi_impl(nsel, sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n, hcol, vcur, ldc, gram, work, stream,
                       GivensArgs{j, kmax, H, cs, sn, g, flag}, JacPre{jac_out, omega, diag});
 }
 
 static int arnoldi_impl(int32_t nsel, const int32_t* sel, double* V, int64_t ldv_sys, int64_t ldv_vec,
                         const int32_t* nv, int32_t kmax, double* w, int64_t ldw, int64_t n, double* hcol,
-                        double* vcur, int64_t ldc, void* work, void* stream, const GivensArgs& GA,
+                        double* vcur, int64_t ldc, double* gram, void* work, void* stream, const GivensArgs& GA,
                         const JacPre& J) {
   MDP_REQUIRE(kmax >= 1 && kmax <= 63, "kmax %d outside [1, 63]", kmax);
   MDP_REQUIRE(n > 0, "empty vectors");
@@ -742,6 +802,28 @@ static int arnoldi_impl(int32_t nsel, const int32_t* sel, double* V, int64_t ldv
   R.out = W.h1;
   R.ostride = kmax + 1;
   R.mode = 0;
+  if (gram) {
+    // MGS from one pass of dot products (the Gram rows of earlier steps stand in for
+    // the sequential projections): V is read twice per step instead of three times
+    R.mode = 3;
+    R.hcol = hcol;
+    R.kmax = kmax;
+    R.nvs = nv;
+    R.gram = gram;
+    R.sel = sel;
+    launch_orth<DOT_SOLVE>(nvmax, grid, st, sel, V, ldv_sys, ldv_vec, nv, w, ldw, n, nullptr, 0, W.partial, pstride,
+                           W.ticket, R);
+    MDP_LAUNCH_CHECK("orth_pass DOT_SOLVE");
+    R.out = W.h2;
+    R.mode = 4;
+    launch_orth<UPD_DOT_NORM>(nvmax, grid, st, sel, V, ldv_sys, ldv_vec, nv, w, ldw, n, W.h1, kmax + 1, W.partial,
+                              pstride, W.ticket, R);
+    MDP_LAUNCH_CHECK("orth_pass UPD_DOT_NORM");
+    ::mdp::launch_k(arnoldi_next_kernel, ew_grid(n, nsel), 256, 0, st, sel, V, ldv_sys, ldv_vec, nv, kmax, w, ldw, n,
+                    hcol, vcur, ldc, GA, J);
+    MDP_LAUNCH_CHECK("mdp_arnoldi");
+    return MDP_OK;
+  }
   launch_orth<DOT>(nvmax, grid, st, sel, V, ldv_sys, ldv_vec, nv, w, ldw, n, nullptr, 0, W.partial, pstride,
                    W.ticket, R);
   MDP_LAUNCH_CHECK("orth_pass DOT");

@@ -115,6 +115,18 @@ def spmv(A, x):
     return A @ x
 
 
+def _gram_storage(nsys, k, f):
+    """Strictly lower Gram rows V_m . V_c of a cycle's basis, [nsys][k+1][k+1]: the
+    Arnoldi step then is modified Gram-Schmidt (krylov.py:138-140) from one pass of
+    dot products (include/mdp_b200.h, mdp_arnoldi).  MDP_ORTH=cgs2 selects the
+    two-pass classical variant (A/B timing only)."""
+    import os
+    import torch
+    if os.environ.get("MDP_ORTH", "mgs") == "cgs2":
+        return None
+    return torch.zeros((nsys, k + 1, k + 1), **f)
+
+
 class _State:
     __slots__ = ("j", "iters", "brk", "conv", "r0", "hist", "H", "cs", "sn", "g", "done", "rel", "beta",
                  "t0", "wall")
@@ -180,6 +192,7 @@ class FgmresEngine:
         self.betad = torch.zeros(nsys, **f)
         wb = self.lib.mdp_arnoldi_work_bytes(nsys, restart, n)
         self.work = torch.zeros(wb // 8 + 1, **f)  # reduction tickets must start at zero
+        self.gram = _gram_storage(nsys, restart, f)
         pin = dict(pin_memory=True)
         self.h_host = torch.zeros(nsys * (restart + 2) + nsys, dtype=torch.float64, **pin)
         self.rn_host = torch.zeros(nsys, dtype=torch.float64, **pin)
@@ -220,7 +233,7 @@ class FgmresEngine:
         _ext.check(self.lib.mdp_arnoldi(ma, sel.data_ptr(), self.V.data_ptr(), (k + 1) * self.ld, self.ld,
                                         nv.data_ptr(), k, self.w.data_ptr(), self.ld, self.n,
                                         self.hcol.data_ptr(), self.vcur.data_ptr(), self.ld,
-                                        self.work.data_ptr(), _ext.stream()))
+                                        _ext.ptr(self.gram), self.work.data_ptr(), _ext.stream()))
 
     def _capture(self, A, Pg, sel, jd, nv, ma, idx):
         """CUDA graph of one Arnoldi step with a graph-safe preconditioner.
@@ -576,6 +589,7 @@ class FixedStepFgmres:
         self.cnt = torch.full((nsys,), m, dtype=torch.int32, device=device)
         wb = self.lib.mdp_arnoldi_work_bytes(nsys, m, n)
         self.work = torch.zeros(wb // 8 + 1, **f)  # reduction tickets must start at zero
+        self.gram = _gram_storage(nsys, m, f)
 
     def run(self, A, P, b, sel, idx, out=None, pre=None):
         """Enqueue the solve of A x = b for the selected systems (no host sync).
@@ -606,7 +620,8 @@ class FixedStepFgmres:
             A(Zj, self.w, sel)
             _ext.check(L.mdp_arnoldi_givens(m, sp_, self.V.data_ptr(), (k + 1) * ld, ld, self.nvs[j].data_ptr(), k,
                                             self.w.data_ptr(), ld, n, self.hcol.data_ptr(), self.vcur.data_ptr(), ld,
-                                            self.work.data_ptr(), j, self.H.data_ptr(), self.cs.data_ptr(),
+                                            _ext.ptr(self.gram), self.work.data_ptr(), j, self.H.data_ptr(),
+                                            self.cs.data_ptr(),
                                             self.sn.data_ptr(), self.g.data_ptr(), self.flag.data_ptr(),
                                             jo if j + 1 < k else None, om, dg, st))
         x = self.x if out is None else out

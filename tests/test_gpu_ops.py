@@ -247,7 +247,8 @@ def test_batched_engine_equals_serial(gpu):
         assert torch.equal(e1.x[0], Xb[i])
 
 
-def test_arnoldi_kernel_orthogonalises(gpu):
+@pytest.mark.parametrize("orth", ["mgs", "cgs2"])
+def test_arnoldi_kernel_orthogonalises(gpu, orth):
     import torch
     from paper_2505_08491_b200 import _ext
     lib = _ext.lib()
@@ -261,15 +262,67 @@ def test_arnoldi_kernel_orthogonalises(gpu):
     nv = torch.tensor([k], dtype=torch.int32, device="cuda")
     H = torch.zeros((1, k + 2), dtype=torch.float64, device="cuda")
     work = torch.zeros(lib.mdp_arnoldi_work_bytes(1, k, n) // 8 + 1, dtype=torch.float64, device="cuda")
+    gram = torch.as_tensor(np.tril(Q.T @ Q, -1), device="cuda").reshape(1, k, k) if orth == "mgs" else None
+    if gram is not None:
+        gram = torch.nn.functional.pad(gram, (0, 1, 0, 1)).contiguous()
     _ext.check(lib.mdp_arnoldi(1, None, V.data_ptr(), (k + 1) * n, n, nv.data_ptr(), k, W.data_ptr(), n, n,
-                               H.data_ptr(), None, 0, work.data_ptr(), _ext.stream()))
+                               H.data_ptr(), None, 0, _ext.ptr(gram), work.data_ptr(), _ext.stream()))
     h = H[0].cpu().numpy()
     assert np.allclose(h[:k], Q.T @ wv, rtol=1e-12, atol=1e-12)
     wr = wv - Q @ (Q.T @ wv)
     assert abs(h[k + 1] - np.linalg.norm(wr)) <= 1e-12 * np.linalg.norm(wr)
     vnext = V[0, k].cpu().numpy()
     assert np.allclose(vnext, wr / np.linalg.norm(wr), atol=1e-12)
-    assert np.max(np.abs(Q.T @ vnext)) <= 1e-13
+    assert np.max(np.abs(Q.T @ vnext)) <= (1e-13 if orth == "cgs2" else 1e-11)
+
+
+@pytest.mark.parametrize("k,nsys", [(3, 2), (30, 1), (50, 2)])
+def test_arnoldi_one_pass_mgs_equals_sequential_mgs(gpu, k, nsys):
+    """The one-pass form (triangular solve over the Gram rows kept by the kernel itself) against
+    the reference's sequential MGS loop (krylov.py:138-141) on a deliberately ill-conditioned
+    sequence: each new direction lies mostly inside the span of the basis, so the Gram rows
+    are far from zero (1e-9..1e-6) and CGS1 would visibly differ from MGS."""
+    import torch
+    from paper_2505_08491_b200 import _ext
+    lib = _ext.lib()
+    n = 20_011
+    ld = (n + 31) // 32 * 32
+    rng = np.random.default_rng(5)
+    V = torch.zeros((nsys, k + 1, ld), dtype=torch.float64, device="cuda")
+    W = torch.zeros((nsys, ld), dtype=torch.float64, device="cuda")
+    H = torch.zeros((nsys, k + 2), dtype=torch.float64, device="cuda")
+    gram = torch.zeros((nsys, k + 1, k + 1), dtype=torch.float64, device="cuda")
+    work = torch.zeros(lib.mdp_arnoldi_work_bytes(nsys, k, n) // 8 + 1, dtype=torch.float64, device="cuda")
+    Vh = np.zeros((nsys, k + 1, n))
+    for s in range(nsys):
+        v0 = rng.standard_normal(n)
+        Vh[s, 0] = v0 / np.linalg.norm(v0)
+    V[:, 0, :n] = torch.as_tensor(Vh[:, 0])
+    for j in range(k):
+        ws = np.zeros((nsys, n))
+        for s in range(nsys):
+            # mostly in span(V): strong cancellation, the hard case for Gram-Schmidt
+            ws[s] = Vh[s, :j + 1].T @ rng.standard_normal(j + 1) * 1e6 + rng.standard_normal(n)
+        W[:, :n] = torch.as_tensor(ws)
+        nv = torch.full((nsys,), j + 1, dtype=torch.int32, device="cuda")
+        _ext.check(lib.mdp_arnoldi(nsys, None, V.data_ptr(), (k + 1) * ld, ld, nv.data_ptr(), k, W.data_ptr(), ld, n,
+                                   H.data_ptr(), None, 0, gram.data_ptr(), work.data_ptr(), _ext.stream()))
+        h = H.cpu().numpy()
+        for s in range(nsys):
+            w = ws[s].copy()
+            hm = np.zeros(j + 1)
+            for i in range(j + 1):  # krylov.py:138-140
+                hm[i] = w @ Vh[s, i]
+                w -= hm[i] * Vh[s, i]
+            hn = np.linalg.norm(w)
+            # the device basis (not the host one) continues the sequence, so rounding does not accumulate
+            Vh[s, j + 1] = V[s, j + 1, :n].cpu().numpy()
+            scale = np.linalg.norm(ws[s])
+            assert np.allclose(h[s, :j + 1], hm, rtol=0, atol=1e-12 * scale), (j, s)
+            assert abs(h[s, k + 1] - hn) <= 1e-9 * hn, (j, s, h[s, k + 1], hn)
+            assert np.allclose(Vh[s, j + 1], w / hn, atol=1e-8), (j, s)
+            g = gram[s, j + 1, :j + 1].cpu().numpy()
+            assert np.allclose(g, Vh[s, :j + 1] @ Vh[s, j + 1], atol=1e-14), (j, s)
 
 
 def _dirichlet_k00(x3, n, h, kO, sO):

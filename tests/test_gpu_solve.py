@@ -47,6 +47,10 @@ def test_solve_coupled_n9_vs_reference(gpu, label, tmp_path):
     assert np.linalg.norm(u3 - g[f"solve_{label}_u3"]) <= 1e-4 * np.linalg.norm(g[f"solve_{label}_u3"])
 
 
+# iteration counts of the reference algorithm on the cfg1 'none' solve under rounding-only changes
+SENSITIVITY_ENVELOPE_NONE = (272, 290)
+
+
 def _cfg1_system():
     from paper_2505_08491_b200 import assembly as A, geometry as G
     graph = G.Graph1D([[0.5, 0.5, 0.1], [0.5, 0.5, 0.9]], [[0, 1]], 0.02, (0,))
@@ -58,10 +62,10 @@ def _cfg1_system():
 def test_solve_cfg1_reference_semantics(gpu, label, tmp_path):
     """cfg1 geometry under the reference's own semantics (reference golden).
 
-    Unpreconditioned inner solve: iteration count within +-2.  Smoothed random
-    CNN: the reference itself hovers at ~1e-6 for >100 iterations before
-    converging at 267; FP64/FP32/TF32 trajectories agree to ~4 digits for the
-    first ~30 iterations and then diverge chaotically, so
+    Unpreconditioned inner solve: iteration count inside the reference algorithm's own
+    rounding envelope.  Smoothed random CNN: the reference itself hovers at ~1e-6 for >100
+    iterations before converging at 267; FP64/FP32/TF32 trajectories agree to ~4 digits
+    for the first ~30 iterations and then diverge chaotically, so
     the gate is early-history agreement plus a final residual near rtol.
     """
     from paper_2505_08491_b200 import harness
@@ -74,17 +78,22 @@ def test_solve_cfg1_reference_semantics(gpu, label, tmp_path):
     want = int(g[f"{label}_iters"])
     h = g[f"{label}_hist"]
     if label == "none":
-        # ~270 iterations over 9 restart cycles: CGS2 vs MGS and summation order
-        # shift the count by a few (measured 278 vs 272); early history is exact
-        # this long solve is sensitive to summation order: counts of 272-285
-        # have been observed across kernel revisions vs the reference's 272
+        # ~270 iterations over 9 restart cycles.  The REFERENCE ALGORITHM ITSELF (FP64, MGS exactly
+        # as krylov.py:138-140) moves between 272 and 290 iterations under changes that only alter
+        # rounding: BLAS ddot 272, pairwise dot 282, correctly rounded dot 290, right-hand side scaled
+        # by 1 + 1..4 ulp 279 / 288 / 273 / 288 (tools/sensitivity_cfg1.py on the oracle,
+        # profiles/r02_sensitivity_cfg1.json).  No implementation that is not bit-identical to
+        # OpenBLAS can hit 272 +- 2, so the gate is that envelope +- 2, convergence, the final true
+        # residual <= rtol and an exact early history.
         assert rep.converged == bool(g[f"{label}_conv"])
-        assert abs(rep.iterations - want) <= 0.1 * want, (rep.iterations, want)
+        assert SENSITIVITY_ENVELOPE_NONE[0] - 2 <= rep.iterations <= SENSITIVITY_ENVELOPE_NONE[1] + 2, (
+            rep.iterations, want)
         assert rep.rel_residual <= 1e-6
         assert np.allclose(rep.residual_history[:20], h[:20], rtol=1e-6)
     else:
-        # the reference hovers at ~1e-6 for >100 iterations and its trajectory
-        # is chaotic under any change of summation order: gate on the early
+        # the reference hovers at ~1e-6 for >100 iterations; in the same experiment its FP64
+        # restatement needs 267 (float32-rounded weights), 540 (float64 weights), > 600 (pairwise
+        # dot) or > 600 (right-hand side scaled by 1 + 1 ulp) iterations: gate on the early
         # history and on staying in the converging regime
         # measured: 1e-5 relative over the first 8 iterations, 3e-3 by iteration 14
         got = np.asarray(rep.residual_history[:15])

@@ -103,15 +103,18 @@ def main():
                 work = torch.zeros(lib.mdp_arnoldi_work_bytes(nb, k, nmax) // 8 + 1, dtype=torch.float64,
                                    device="cuda")
 
-                def arn():
-                    _ext.check(lib.mdp_arnoldi(nb, None, V.data_ptr(), (k + 1) * prob.ld, prob.ld, nv.data_ptr(), k,
-                                               W.data_ptr(), prob.ld, nmax, H.data_ptr(), None, 0, work.data_ptr(),
-                                               _ext.stream()))
-                ms = timed(arn, a.reps, flush)
+                gram = torch.zeros((nb, k + 1, k + 1), dtype=torch.float64, device="cuda")
                 byt = (2 * k + 3) * nmax * 8 * nb
-                r["arnoldi30"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9,
-                                  "frac_hbm": byt / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], "bytes": byt,
-                                  "note": "CGS2: V read 3x; bytes = survey formula (2k+3) N 8"}
+                for tag, gr, note in (("arnoldi30", gram, "one-pass MGS: V read 2x"),
+                                      ("arnoldi30_cgs2", None, "CGS2: V read 3x")):
+                    def arn():
+                        _ext.check(lib.mdp_arnoldi(nb, None, V.data_ptr(), (k + 1) * prob.ld, prob.ld, nv.data_ptr(),
+                                                   k, W.data_ptr(), prob.ld, nmax, H.data_ptr(), None, 0,
+                                                   _ext.ptr(gr), work.data_ptr(), _ext.stream()))
+                    ms = timed(arn, a.reps, flush)
+                    r[tag] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9,
+                              "frac_hbm": byt / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], "bytes": byt,
+                              "note": note + "; bytes = survey formula (2k+3) N 8"}
                 del V, W
             # CNN forward (pack -> U-Net -> rescale), batch nb
             D = torch.rand((nb, n3), dtype=torch.float64, device="cuda")
