@@ -321,11 +321,106 @@ __global__ void __launch_bounds__(128) orth_pass_kernel(const int32_t* sel, cons
   __syncthreads();
   for (int k = threadIdx.x; k < nk; k += blockDim.x)
     mine[k] = ((wsum[0][k] + wsum[1][k]) + wsum[2][k]) + wsum[3][k];
-  if (BOTH && threadIdx.x == 0)
+  if (BOTH && threadIdx.x == nk)  // the thread that hands slot nk to finish_reduction
     mine[nk] = ((wsum[0][NACC] + wsum[1][NACC]) + wsum[2][NACC]) + wsum[3][NACC];
   RedOut Rl = R;
   Rl.nk = BOTH ? nk + 1 : nk;
   finish_reduction<MODE == DOT_SOLVE ? NV : 0>(partial, pstride, ticket, Rl, mine);
+}
+
+// Wide bases (33..64 vectors, restart 50): the plain pass needs one accumulator per
+// vector and thread (255 registers at 64, 8 warps per SM).  Here the four warps of
+// a block split the BASIS (warp q owns vectors [16 q, 16 q + 16)) and share the
+// elements: a tile is 64 elements, one pair per lane.  A warp loads its 16 basis
+// values of the tile ONCE and keeps them in registers for both the update and the
+// dot products; the update's partial sums meet in shared memory (fixed warp order),
+// so V is read once per pass whatever nv is, and warps whose vectors lie beyond nv
+// issue no loads.  DOT_SOLVE: a = V^T w.  UPD_DOT_NORM: w' = w - V c, V^T w', ||w'||^2.
+template <int MODE>
+__global__ void __launch_bounds__(128) orth_wide_kernel(const int32_t* sel, const double* __restrict__ V,
+                                                        int64_t ldv_sys, int64_t ldv_vec,
+                                                        const int32_t* __restrict__ nvs, double* w, int64_t ldw,
+                                                        int64_t n, const double* __restrict__ coef, int cstride,
+                                                        double* __restrict__ partial, int pstride,
+                                                        unsigned int* ticket, RedOut R, int64_t chunk) {
+  MDP_PDL_ENTER();
+  constexpr bool UPD = MODE == UPD_DOT_NORM;
+  constexpr int GS = 16;
+  __shared__ double csh[64];
+  __shared__ double2 part[2][4][32];
+  __shared__ double mine[65];
+  const int i = blockIdx.y;
+  const int s = sys_of(sel, i);
+  const int nv = nvs[i];
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const int64_t e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
+  const double* Vs = V + s * ldv_sys + (int64_t)(GS * q) * ldv_vec;
+  double* ws = w + s * ldw;
+  const int mynv = min(GS, max(0, nv - GS * q));  // vectors this warp owns
+  if (UPD) {
+    for (int k = threadIdx.x; k < 64; k += blockDim.x) csh[k] = k < nv ? coef[i * cstride + k] : 0.0;
+    __syncthreads();
+  }
+  double acc[GS];
+  double accn = 0.0;
+#pragma unroll
+  for (int k = 0; k < GS; ++k) acc[k] = 0.0;
+  int buf = 0;
+  for (int64_t e = e0 + 2 * lane; e < e1 + 2 * lane; e += 64) {  // uniform trip count (block barriers inside)
+    const bool in0 = e < e1, in1 = e + 1 < e1;
+    double2 w2 = make_double2(0.0, 0.0);
+    if (in1) w2 = *reinterpret_cast<const double2*>(ws + e);
+    else if (in0) w2.x = ws[e];
+    double2 vv[GS];
+#pragma unroll
+    for (int k = 0; k < GS; ++k) {
+      vv[k] = make_double2(0.0, 0.0);
+      if (k < mynv) {
+        if (in1) vv[k] = __ldg(reinterpret_cast<const double2*>(Vs + k * ldv_vec + e));
+        else if (in0) vv[k].x = __ldg(Vs + k * ldv_vec + e);
+      }
+    }
+    if (UPD) {
+      double2 p = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < GS; ++k) {
+        p.x = fma(csh[GS * q + k], vv[k].x, p.x);
+        p.y = fma(csh[GS * q + k], vv[k].y, p.y);
+      }
+      part[buf][q][lane] = p;
+      __syncthreads();
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        w2.x -= part[buf][g][lane].x;
+        w2.y -= part[buf][g][lane].y;
+      }
+      buf ^= 1;
+      if (q == 0) {
+        if (in1) *reinterpret_cast<double2*>(ws + e) = w2;
+        else if (in0) ws[e] = w2.x;
+        accn = fma(w2.x, w2.x, accn);
+        accn = fma(w2.y, w2.y, accn);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < GS; ++k) {
+      acc[k] = fma(vv[k].x, w2.x, acc[k]);
+      acc[k] = fma(vv[k].y, w2.y, acc[k]);
+    }
+  }
+  warp_sums<GS>(acc);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < GS; ++k) mine[GS * q + k] = acc[k];
+  __syncthreads();  // mine[0..64) complete before slot nv takes the norm
+  if (UPD && q == 0) {
+    for (int o = 16; o > 0; o >>= 1) accn += __shfl_xor_sync(0xffffffffu, accn, o);
+    if (lane == 0) mine[nv] = accn;
+  }
+  __syncthreads();
+  RedOut Rl = R;
+  Rl.nk = UPD ? nv + 1 : nv;
+  finish_reduction<MODE == DOT_SOLVE ? 64 : 0>(partial, pstride, ticket, Rl, mine);
 }
 
 // V[s][nv] = w / hn  (and vcur), exact division like krylov.py:165
@@ -378,6 +473,9 @@ static void launch_orth(int nv_max, dim3 grid, cudaStream_t st, const int32_t* s
                                                     coef, cstride, partial, pstride, ticket, R, red_chunk(n))
   if (MODE == NORM) {
     MDP_ORTH(0);
+  } else if ((MODE == DOT_SOLVE || MODE == UPD_DOT_NORM) && nv_max > 32) {
+    ::mdp::launch_k(orth_wide_kernel<(MODE == DOT_SOLVE || MODE == UPD_DOT_NORM) ? MODE : (int)DOT_SOLVE>, grid, 128, 0, st,
+                    sel, V, ldv_sys, ldv_vec, nvs, w, ldw, n, coef, cstride, partial, pstride, ticket, R, red_chunk(n));
   } else if (nv_max <= 4) {
     MDP_ORTH(4);
   } else if (nv_max <= 8) {

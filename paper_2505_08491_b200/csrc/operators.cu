@@ -283,7 +283,7 @@ template <int N, int RY, bool JAC, bool DIR, bool EDGE>
 __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* __restrict__ yp,
                                                   const double* __restrict__ jrp, const double* __restrict__ dgp,
                                                   double omega, int n, int i, int j, int z0, int z1,
-                                                  const StencilCoef& K, const double* stg, int sw,
+                                                  const StencilCoef& K, const double* stg, int sw, int swj,
                                                   uint64_t* full, uint64_t* empty, int r_lo, int r_hi) {
   using namespace async;
   constexpr int NR = RY + 2;
@@ -327,12 +327,23 @@ __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* 
       const int kc = k < 0 ? 0 : (k > n - 1 ? n - 1 : k);  // plane the producer copied
       const bool pok = k >= 0 && k < n && !(DIR && (k == 0 || k == n - 1));
       mbar_wait(&full[u], par);
-      const double* b = stg + (size_t)u * sw + ((kc * nn + r_lo * n) & 1);
+      const double* b = stg + (size_t)u * (sw + 2 * swj) + ((kc * nn + r_lo * n) & 1);
       double c[NR], lr[NR];
 #pragma unroll
       for (int a = 0; a < NR; ++a) {
         c[a] = b[roff[a]];
         lr[a] = fma(mL, b[roff[a] - 1], mR * b[roff[a] + 1]);
+      }
+      // Jacobi epilogue operands of the plane emitted in this step (k - 1): the
+      // producer staged r and diag(C) of this band beside the x plane
+      double jv[JAC ? RY : 1], dv[JAC ? RY : 1];
+      if (JAC) {
+        const double* jb = stg + (size_t)u * (sw + 2 * swj) + sw + (((k - 1) * nn + j * n) & 1) + ic;
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          jv[r] = jb[r * n];
+          dv[r] = jb[swj + r * n];
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[u]);
@@ -377,7 +388,7 @@ __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* 
         double out = DIR ? (Um[r] + un) + Ck[r] : fma(sig, Ck[r], Um[r] + un);
         if (DIR && (rbnd[r] || pbnd)) out = xo[r];
         if (emit && rout[r]) {
-          if (JAC) out = xo[r] + (omega * (jrp[ko * nn + obase + r * n] - out)) / dgp[ko * nn + obase + r * n];
+          if (JAC) out = xo[r] + (omega * (jv[r] - out)) / dv[r];
           yrow[r * n] = out;
         }
         Un[r] = un;
@@ -415,7 +426,9 @@ __global__ void __launch_bounds__(256, STENCIL3_MINB) stencil3_kernel(const mdp_
   uint64_t* empty = full + kSt3;
   // stage: one pad double in front (x-neighbour reads of column -1 stay in range), then the band
   double* stg = reinterpret_cast<double*>(smem3 + 16 * kSt3) + 2;
-  const int sw = (NR * n + 4 + 1) & ~1;  // stage stride in doubles (16-byte multiple)
+  const int sw = (NR * n + 4 + 1) & ~1;  // x-band stride in doubles (16-byte multiple)
+  const int swj = JAC ? ((RY * n + 3) & ~1) : 0;  // r / diag(C) bands of the emitted plane (Jacobi epilogue)
+  const int sws = sw + 2 * swj;              // whole stage
   const int tiles_x = (n + 31) / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bands = (n + RY - 1) / RY;
@@ -434,7 +447,7 @@ __global__ void __launch_bounds__(256, STENCIL3_MINB) stencil3_kernel(const mdp_
   }
   // zero the ring once: neighbour reads past a band's copied bytes (masked
   // by 0) must see finite values
-  for (int t = threadIdx.x; t < kSt3 * sw + 2; t += blockDim.x) stg[t - 2] = 0.0;
+  for (int t = threadIdx.x; t < kSt3 * sws + 2; t += blockDim.x) stg[t - 2] = 0.0;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes before the async-proxy copies
   __syncthreads();
   const double* xp = x + (int64_t)s * ldx;
@@ -445,16 +458,29 @@ __global__ void __launch_bounds__(256, STENCIL3_MINB) stencil3_kernel(const mdp_
     if (lane == 0) {
       const int nn = n * n;
       const uint32_t cnt = (uint32_t)(r_hi - r_lo + 1) * n;
+      const uint32_t cntj = (uint32_t)(min(RY, n - j)) * n;
+      const double* jsrc = JAC ? jr + (int64_t)s * ldy : nullptr;
+      const double* dsrc = JAC ? P.diag_c + (int64_t)s * ldy : nullptr;
       for (int st = 0; st < nsteps; ++st) {
         const int slot = st % kSt3;
         if (st >= kSt3) mbar_wait(&empty[slot], (uint32_t)(((st / kSt3) - 1) & 1));
         int k = z0 - 1 + st;
+        const int ko = k - 1;  // plane emitted at this step (from z0 on)
         k = k < 0 ? 0 : (k > n - 1 ? n - 1 : k);
         const int e0 = k * nn + r_lo * n;
         const int sh = e0 & 1;
         const uint32_t bytes = ((cnt + sh) * 8 + 15) & ~15u;
-        mbar_expect_tx(&full[slot], bytes);
-        bulk_load(stg + (size_t)slot * sw, xp + (e0 - sh), bytes, &full[slot]);
+        if (JAC && ko >= z0) {
+          const int ej = ko * nn + j * n;
+          const int shj = ej & 1;
+          const uint32_t bj = ((cntj + shj) * 8 + 15) & ~15u;
+          mbar_expect_tx(&full[slot], bytes + 2 * bj);
+          bulk_load(stg + (size_t)slot * sws + sw, jsrc + (ej - shj), bj, &full[slot]);
+          bulk_load(stg + (size_t)slot * sws + sw + swj, dsrc + (ej - shj), bj, &full[slot]);
+        } else {
+          mbar_expect_tx(&full[slot], bytes);
+        }
+        bulk_load(stg + (size_t)slot * sws, xp + (e0 - sh), bytes, &full[slot]);
       }
     }
     return;
@@ -470,7 +496,7 @@ __global__ void __launch_bounds__(256, STENCIL3_MINB) stencil3_kernel(const mdp_
   const int lo = dir ? 1 : 0, hi = dir ? n - 2 : n - 1;
   const bool edge = (j - 1 < lo) || (j + RY > hi);
 #define MDP_ST3(D, E) \
-  stencil3_consumer<N, RY, JAC, D, E>(P, yp, jrp, dgp, omega, n, i, j, z0, z1, K, stg, sw, full, empty, r_lo, r_hi)
+  stencil3_consumer<N, RY, JAC, D, E>(P, yp, jrp, dgp, omega, n, i, j, z0, z1, K, stg, sw, swj, full, empty, r_lo, r_hi)
   if (dir) {
     if (edge) MDP_ST3(true, true); else MDP_ST3(true, false);
   } else {
@@ -670,7 +696,9 @@ static int launch_stencil3(const mdp_problem* p, int32_t nsel, const int32_t* se
   const int bands = ceil_div(n, RY);
   const int threads = 32 * (tiles_x + 1);
   const size_t sw = (size_t)(((RY + 2) * n + 4 + 1) & ~1);
-  const size_t smem = 16 * (size_t)S + (size_t)S * sw * 8 + 32;
+  const size_t swj = jr ? (size_t)((RY * n + 3) & ~1) : 0;  // Jacobi: r and diag(C) bands ride in the stage
+  const size_t smem = 16 * (size_t)S + (size_t)S * (sw + 2 * swj) * 8 + 32;
+  MDP_REQUIRE(smem <= 200 * 1024, "stencil stage ring of %zu bytes exceeds shared memory (n = %d, RY = %d)", smem, n, RY);
   // z-chunks: ~4 waves of blocks (occupancy from shared memory, <= 8 blocks/SM)
   int per_sm = (int)((200 * 1024) / smem);
   per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
