@@ -10,6 +10,8 @@
 //           by the parity tests to localise tensor-core errors
 // enc1a (Cin=2), the stride-2 transposed convs and the 1x1 heads are
 // memory-bound and run on CUDA cores in both paths.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "unet_layout.cuh"
 
@@ -19,12 +21,24 @@ namespace mdp {
 // input pack: xin[b][v] = (r_s[v] / ||r_s||, d_s[v])   (training.py:312-318)
 __global__ void pack_input_kernel(const int32_t* sel, const double* __restrict__ r, int64_t ld,
                                   const double* __restrict__ rnorm, const double* __restrict__ dist,
-                                  int64_t ldd, float2* __restrict__ xin, int64_t nvox) {
+                                  int64_t ldd, float2* __restrict__ xin, int64_t nvox, int S, int shifted) {
   MDP_PDL_ENTER();
   const int b = blockIdx.y;
   const int s = sys_of(sel, b);
   double nr = rnorm[b];
   double den = nr != 0.0 ? nr : 1.0;
+  if (shifted) {
+    // tensor-core enc1a (tc_enc1a): quad of voxel x = (r, d)[x] | (r, d)[x+1] (zero past the row end), TF32-rounded
+    float4* x4 = reinterpret_cast<float4*>(xin);
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
+         v += (int64_t)gridDim.x * blockDim.x) {
+      const bool nxt = (int)(v % S) + 1 < S;
+      const double r0 = r[s * ld + v] / den, r1 = nxt ? r[s * ld + v + 1] / den : 0.0;
+      const double d0 = dist[s * ldd + v], d1 = nxt ? dist[s * ldd + v + 1] : 0.0;
+      x4[b * nvox + v] = tf32_round4(make_float4((float)r0, (float)d0, (float)r1, (float)d1));
+    }
+    return;
+  }
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
        v += (int64_t)gridDim.x * blockDim.x) {
     double rv = r[s * ld + v] / den;
@@ -338,6 +352,16 @@ static int launch_tconv(int nb, const float4* in, int in_cq, int cin, int cout, 
   return MDP_OK;
 }
 
+// A/B switch: MDP_ENC1A_TC=0 keeps enc1a on CUDA cores at every size
+static bool enc1a_cuda_cores() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MDP_ENC1A_TC");
+    v = (e && e[0] == '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 UnetPlan unet_plan(int n, int nb, int path) {
   UnetPlan p;
   p.n = n;
@@ -350,7 +374,7 @@ UnetPlan unet_plan(int n, int nb, int path) {
     off += (bytes + 255) & ~(size_t)255;
     return o;
   };
-  p.o_xin = take((size_t)nb * N * sizeof(float2));
+  p.o_xin = take((size_t)nb * N * sizeof(float4));  // float2 (r, d), or the x-shifted quads of tc_enc1a
   p.o_a1 = take((size_t)nb * 4 * N * 16);
   p.o_c1 = take((size_t)nb * 16 * N * 16);
   p.o_c2 = take((size_t)nb * 32 * M * 16);
@@ -430,14 +454,18 @@ extern "C" int mdp_unet_apply(const mdp_unet* net, int32_t nb, const int32_t* se
   const int64_t N = (int64_t)n * n * n;
   const int tf = path == 0;  // round stored activations to TF32 on the tensor-core path
   int rc;
+  // wide grids on the tensor-core path: enc1a as a K = 8 MMA per (dy, halo plane) over x-shifted input quads
+  const int tc_enc = path == 0 && n >= TC_ENC1A_MIN_S && !enc1a_cuda_cores();
 
   {
     int bx = ceil_div(N, 256);
     bx = bx > 8 * sm_count() ? 8 * sm_count() : bx;
-    ::mdp::launch_k(pack_input_kernel, dim3(bx, nb), 256, 0, st, sel, r, ld, rnorm, dist, ldd, xin, N);
+    ::mdp::launch_k(pack_input_kernel, dim3(bx, nb), 256, 0, st, sel, r, ld, rnorm, dist, ldd, xin, N, n, tc_enc);
     MDP_LAUNCH_CHECK("pack_input_kernel");
   }
-  if (n >= 64)  // wide grids: two voxels per thread; small latency-bound grids: one
+  if (tc_enc) {
+    if ((rc = tc_enc1a(nb, n, (const float4*)xin, net->w[0], net->b[0], a1, 4, 0, st))) return rc;
+  } else if (n >= 64)  // wide grids: two voxels per thread; small latency-bound grids: one
     ::mdp::launch_k(enc1a_kernel<2>, dim3(ceil_div((int64_t)((n + 1) / 2) * n * n, 128), nb), 128, 0, st, xin, n,
                     net->w[0], net->b[0], a1, tf);
   else

@@ -31,6 +31,10 @@ struct HeadArgs {  // dec1 -> head1 -> head2 -> scale (EPI_HEAD)
 int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int in_q0, const float* w,
              const float* bias, int relu, float4* out, int out_cq, int out_q0, int epi, const HeadArgs* head,
              void* scratch, size_t scratch_bytes, cudaStream_t st);
+// enc1a (2 -> 16) on tensor cores for wide grids (S >= TC_ENC1A_MIN_S); xin from pack_input_kernel mode 1
+constexpr int TC_ENC1A_MIN_S = 64;
+int tc_enc1a(int nb, int S, const float4* xin, const float* w, const float* bias, float4* out, int out_cq,
+             int out_q0, cudaStream_t st);
 // transposed conv k=2 s=2 (+ bias, ReLU, TF32 rounding, output-padding
 // planes) on tensor cores; w packed [tap][quad][Cout][4] (neural.pack_tconv path 0)
 int tc_tconv(int nb, const float4* in, int in_cq, int cin, int cout, int Sin, int op, const float* w,

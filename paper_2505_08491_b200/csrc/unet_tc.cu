@@ -20,8 +20,8 @@
 // B operand: weights pre-packed per (chunk, tap) as [quad][Cout][4 floats]
 // (K-major no-swizzle) and streamed with 1-D bulk copies.
 //
-// Warp roles (256 threads): w0 weight (bulk) producer, w3 halo (TMA)
-// producer, w1 MMA issuer, w2 TMEM allocator, w4..w7 epilogue (TMEM -> registers -> bias/ReLU/TF32 round ->
+// Warp roles (384 threads): w0 weight (bulk) producer, w3 halo (TMA)
+// producer, w1 MMA issuer, w2 TMEM allocator, w4..w11 epilogue (TMEM -> registers -> bias/ReLU/TF32 round ->
 // global, optional fused 2x2x2 max-pool).  Two TMEM accumulator buffers let
 // the epilogue of tile t overlap the MMAs of tile t+1.
 #include <cuda.h>
@@ -47,6 +47,20 @@ struct Brick {
   static constexpr int QUAD_BYTES = HZ * HY * HX * 16;  // one quad plane of the halo brick
 };
 
+// Optional clock64 trace of CTA 0 (build with -DCONV_TRACE; tools/conv_trace.py): per tile the
+// cycles at which each role passed its waits, for the launch whose (cin, cout) was selected.
+#ifdef CONV_TRACE
+__device__ long long g_trace[16 + 6 * 48 * 4];
+__device__ int g_trace_sel[2];
+#define TR(slot, ti, k)                                                                              \
+  do {                                                                                               \
+    if (blockIdx.x == 0 && (ti) < 48 && A.cin == g_trace_sel[0] && A.cout == g_trace_sel[1])         \
+      g_trace[16 + ((slot) * 48 + (ti)) * 4 + (k)] = clock64();                                      \
+  } while (0)
+#else
+#define TR(slot, ti, k) do { } while (0)
+#endif
+
 struct ConvArgs {
   int nb, S, cin, cout, cqc, nchunk;
   int nsplit, ncol;  // output channels split over nsplit CTAs of ncol each (small layers)
@@ -65,6 +79,8 @@ struct ConvArgs {
   int tps;       // taps (fold: (dy,dx) units) per weight stage (one mbarrier handshake per stage)
   int fold;      // Cout == 32: the 3 z-taps of one (dy,dx) are one N = 3*32 weight block (see issue_stage_fold)
   uint32_t tmem_cols;
+  int pair;           // enc1a (Cin = 2): x-shifted input quads, one K = 8 MMA per (dy, halo plane) (see issue_stage_pair)
+  const float* wraw;  // pair: the raw [16][2][27] filter, packed into shared memory by the kernel itself
   HeadArgs head;
 };
 
@@ -178,6 +194,44 @@ __device__ __forceinline__ void issue_stage_fold(uint32_t a_lo, uint32_t a_hi, u
   accf = 1u;
 }
 
+// enc1a (Cin = 2 -> 16): the input quad of voxel x is (r[x], d[x], r[x+1], d[x+1]), so with
+// LBO = 16 B (the next x-voxel) one K = 8 step reads (r,d)[x-1], (r,d)[x], (r,d)[x], (r,d)[x+1]:
+// all three dx taps of one (dz,dy) (weight slots 2-3 are zero).  With the z-tap fold the whole
+// 54-term filter is 3 (dy) x (ZP+2) (halo planes) MMAs per brick; the layer is store-bound.
+template <int ZP>
+__device__ __forceinline__ void issue_stage_pair(uint32_t a_lo, uint32_t a_hi, uint32_t b_lo, uint32_t b_hi,
+                                                 uint32_t b_unit16, uint32_t dcol, uint32_t ncol,
+                                                 const uint32_t* idesc_n, uint32_t& accf) {
+  constexpr int NINIT = ZP == 2 ? 1 : 2;
+  const uint32_t acc0 = accf;
+#pragma unroll
+  for (int tt = 0; tt < 3; ++tt) {
+#pragma unroll
+    for (int h = 0; h < ZP + 2; ++h) {
+      const int hp = fold_hp<ZP>(h);
+      const int zlo = hp - 2 > 0 ? hp - 2 : 0, zhi = hp < ZP - 1 ? hp : ZP - 1;
+      const int ndz = zhi - zlo + 1, dz_lo = hp - zhi;
+      const uint64_t ad = ((uint64_t)a_hi << 32) | (a_lo + (uint32_t)(tt * HX + hp * HY * HX));
+      const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo + tt * b_unit16 + dz_lo * ncol);
+      mma_tf32(dcol + (uint32_t)(ZP - 1 - zhi) * ncol, ad, bd, idesc_n[ndz - 1], (tt == 0 && h < NINIT) ? acc0 : 1u);
+    }
+  }
+  accf = 1u;
+}
+
+// One elected lane of a converged warp.  Unlike `lane == 0`, the compiler knows a single thread
+// runs the guarded code, so descriptors move to uniform registers without a per-MMA
+// ELECT / R2UR.BROADCAST / BRA.U.ANY waterfall loop (measured: ~70-110 -> cycles per issued MMA).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -220,7 +274,7 @@ __device__ __forceinline__ void decode_tile(const ConvArgs& A, int tile, int& b,
 }
 
 template <int ZP>
-__global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(384, 1) conv3_tc_kernel(const __grid_constant__ CUtensorMap tmap,
                                                           const __grid_constant__ CUtensorMap wmap,
                                                           const ConvArgs A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -237,6 +291,9 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
   uint32_t* tmem_slot = (uint32_t*)(t_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef CONV_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0 && A.cin == g_trace_sel[0] && A.cout == g_trace_sel[1]) g_trace[0] = clock64();
+#endif
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < A.na; ++i) {
       mbar_init(&a_full[i], 1);
@@ -248,7 +305,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], 128);
+      mbar_init(&t_empty[i], 256);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
@@ -268,16 +325,17 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
   // stages without waiting for it either
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (warp != 0) asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int nunits = A.fold ? 9 : 27;
+  const int nunits = A.pair ? 3 : (A.fold ? 9 : 27);
 
   if (warp == 3) {
     if (lane == 0) {  // ---------------- A producer: halo bricks, one TMA box per 32-channel chunk
-      int as = 0, ap = 0;
-      for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
+      int as = 0, ap = 0, ti = 0;
+      for (int tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x, ++ti) {
         int b, x0, y0, z0, n0, ks;
         decode_tile<ZP>(A, tile, b, x0, y0, z0, n0, ks);
         for (int c = ks * A.cps; c < (ks + 1) * A.cps; ++c) {
           mbar_wait(&a_empty[as], ap ^ 1);
+          if (c == ks * A.cps) TR(0, ti, 0);
           mbar_expect_tx(&a_full[as], A.a_bytes);
           // inner box row = 10 voxels x 4 channels (160 B); coordinate -4 floats = voxel x0-1
           tma_load_4d(sA + (size_t)as * A.a_bytes, &tmap, &a_full[as], 4 * (x0 - 1), y0 - 1, z0 - 1,
@@ -286,6 +344,19 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
         }
       }
     }
+  } else if (warp == 0 && A.pair) {
+    // ---------------- pair mode: the 54 x 16 filter is packed here as [dy][kq][dz][cout][4]
+    // (kq 0 = (w(dx0,r), w(dx0,d), 0, 0), kq 1 = (w(dx1,r), w(dx1,d), w(dx2,r), w(dx2,d))), TF32-rounded
+    float* wb = reinterpret_cast<float*>(sB);
+    for (int t = lane; t < 3 * 2 * 3 * 16 * 4; t += 32) {
+      const int e = t & 3, c = (t >> 2) & 15, dz = (t >> 6) % 3, kq = ((t >> 6) / 3) & 1, dy = (t >> 6) / 6;
+      const int ch = e & 1, dx = kq == 0 ? 0 : 1 + (e >> 1);
+      const float v = (kq == 0 && e >= 2) ? 0.f : A.wraw[(c * 2 + ch) * 27 + (dz * 3 + dy) * 3 + dx];
+      wb[t] = tf32_round(v);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&b_full[0]);
   } else if (warp == 0) {
     if (lane == 0) {  // ---------------- B producer: weight tiles per (chunk, tap)
       int bs = 0, bp = 0;
@@ -317,10 +388,10 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    if (elect_one()) {  // ---------------- MMA issuer
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(A.ncol >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
-      const uint32_t lbo_a = Brick<ZP>::QUAD_BYTES, sbo_a = HX * 16;
+      const uint32_t lbo_a = A.pair ? 16u : Brick<ZP>::QUAD_BYTES, sbo_a = HX * 16;
       const uint32_t lbo_b = A.ncol * 16 * (A.fold ? 3 : 1), sbo_b = 128;
       uint32_t idesc_n[3];  // fold: N = 1, 2, 3 x ncol
       for (int k = 0; k < 3; ++k) idesc_n[k] = (idesc & ~(0x3Fu << 17)) | ((uint32_t)(((k + 1) * A.ncol) >> 3) << 17);
@@ -330,11 +401,13 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
         const int buf = li & 1;
         mbar_wait(&t_empty[buf], ((li >> 1) & 1) ^ 1);
         fence_after();
+        TR(1, li, 0);
         const uint32_t dcol = tmem + (uint32_t)(buf * ZP * A.ncol);
         uint32_t accf = 0u;  // the tile's first MMA overwrites the accumulator
         for (int c = 0; c < A.cps; ++c) {
           mbar_wait(&a_full[as], ap);
           fence_after();
+          if (c == 0) TR(1, li, 1);
           const uint32_t abase = a0 + as * A.a_bytes;
           for (int t0 = 0; t0 < nunits; t0 += A.tps) {
             if (!A.resident || li == 0) {
@@ -347,7 +420,9 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
             const uint32_t b_lo = (uint32_t)bd0, b_hi = (uint32_t)(bd0 >> 32);
             const uint32_t b_tap16 = (uint32_t)(A.cqc * A.ncol * (A.fold ? 3 : 1));  // one unit's weights / 16 B
             const uint32_t b_ks16 = (uint32_t)(2 * A.ncol * (A.fold ? 3 : 1));         // (2 * lbo_b) / 16
-            if (A.fold) {
+            if (A.pair) {
+              issue_stage_pair<ZP>(a_lo, a_hi, b_lo, b_hi, 6u * A.ncol, dcol, A.ncol, idesc_n, accf);
+            } else if (A.fold) {
               switch (A.tps) {
                 case 9: issue_stage_fold<9, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc_n, accf); break;
                 case 3: issue_stage_fold<3, ZP>(a_lo, a_hi, b_lo, b_hi, b_tap16, b_ks16, dcol, A.ncol, idesc_n, accf); break;
@@ -368,10 +443,14 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           if (++as == A.na) { as = 0; ap ^= 1; }
         }
         mma_commit(&t_full[buf]);
+        TR(1, li, 2);
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue
-    const int ew = warp - 4;
+    // 8 warps: warp w reads TMEM lane quarter w % 4; the two warps of a quarter split the
+    // brick's (plane, 16-column group) items by parity (the epilogue is a dependent
+    // instruction chain per warp: ncu showed the store-heavy layers bound by it at 4 warps)
+    const int ew = (warp - 4) & 3, eh = (warp - 4) >> 2;
     const int row = ew * 32 + lane;
     const int ly = row >> 3, lx = row & 7;
     const uint32_t lane_addr = (uint32_t)(ew * 32) << 16;
@@ -386,6 +465,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
       decode_tile<ZP>(A, tile, b, x0, y0, z0, n0, ks);
       mbar_wait(&t_full[buf], (li >> 1) & 1);
       fence_after();
+      if (lane == 0 && ew == 0) TR(2 + eh, li, 0);
       const uint32_t dcol = tmem + lane_addr + (uint32_t)(buf * ZP * A.ncol);
       const int q0 = A.out_q0 + n0 / 4;
       const int gx = x0 + lx, gy = y0 + ly;
@@ -396,6 +476,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           const int gz = z0 + zp;
           const bool ok = gx < S && gy < S && gz < S;
           for (int cg = 0; cg < A.ncol / 16; ++cg) {
+            if (((zp * (A.ncol / 16) + cg) & 1) != eh) continue;
             float v[16];
             tmem_ld16(dcol + zcol(zp) + cg * 16, v);
             if (ok) {
@@ -413,6 +494,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
         const double rn = H.rnorm[b];
 #pragma unroll
         for (int zp = 0; zp < ZP; ++zp) {
+          if ((zp & 1) != eh) continue;
           const int gz = z0 + zp;
           const bool ok = gx < S && gy < S && gz < S;
           float v[32];
@@ -438,6 +520,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           const int pz = (z0 >> 1) + pp;
           const bool writer = ((lane & 1) == 0) && ((ly & 1) == 0) && px < So && py < So && pz < So;
           for (int cg = 0; cg < A.ncol / 16; ++cg) {
+            if (((pp * (A.ncol / 16) + cg) & 1) != eh) continue;
             float v0[16], v1[16];
             tmem_ld16(dcol + zcol(2 * pp) + cg * 16, v0);
             tmem_ld16(dcol + zcol(2 * pp + 1) + cg * 16, v1);
@@ -465,6 +548,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
           const int gz = z0 + zp;
           const bool ok = gx < S && gy < S && gz < S;
           for (int cg = 0; cg < A.ncol / 16; ++cg) {
+            if (((zp * (A.ncol / 16) + cg) & 1) != eh) continue;
             float v[16];
             tmem_ld16(dcol + zcol(zp) + cg * 16, v);
 #pragma unroll
@@ -485,6 +569,7 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
         }
       }
       fence_before();
+      if (lane == 0 && ew == 0) TR(2 + eh, li, 1);
       mbar_arrive(&t_empty[buf]);
     }
   }
@@ -495,6 +580,9 @@ __global__ void __launch_bounds__(256, 1) conv3_tc_kernel(const __grid_constant_
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(A.tmem_cols));
   }
+#ifdef CONV_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0 && A.cin == g_trace_sel[0] && A.cout == g_trace_sel[1]) g_trace[1] = clock64();
+#endif
 }
 
 // Fixed-order sum of the ksplit partials + bias + ReLU (+ 2x2x2 max pool) +
@@ -670,7 +758,7 @@ __global__ void __launch_bounds__(192, 1) tconv_tc_kernel(const TconvArgs T) {
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
+    if (elect_one()) {  // ---- MMA issuer
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(T.cout >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
       const uint32_t b0 = smem_u32(sB);
@@ -740,6 +828,23 @@ __global__ void __launch_bounds__(192, 1) tconv_tc_kernel(const TconvArgs T) {
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(T.tmem_cols));
 }
 
+}  // namespace tc
+}  // namespace mdp
+#ifdef CONV_TRACE
+extern "C" int mdp_conv_trace_select(int cin, int cout) {
+  int sel[2] = {cin, cout};
+  cudaMemset(nullptr, 0, 0);
+  static long long zero[16 + 6 * 48 * 4] = {0};
+  cudaMemcpyToSymbol(mdp::tc::g_trace, zero, sizeof(zero));
+  return (int)cudaMemcpyToSymbol(mdp::tc::g_trace_sel, sel, sizeof(sel));
+}
+extern "C" int mdp_conv_trace_read(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, mdp::tc::g_trace, sizeof(long long) * (16 + 6 * 48 * 4));
+}
+#endif
+namespace mdp {
+namespace tc {
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -786,6 +891,15 @@ static void tc_split(int nb, int S, int cin, int cout, int& nsplit, int& ksplit)
         ksplit = k;
         break;
       }
+}
+
+static void conv3_smem_attr() {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tc::conv3_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+    cudaFuncSetAttribute(tc::conv3_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+    attr_set = true;
+  }
 }
 
 size_t tc_conv3_scratch_bytes(int nb, int S, int cin, int cout) {
@@ -905,18 +1019,13 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   }
 
   const size_t smem = 1024 + (size_t)A.na * A.a_bytes + (size_t)nbs * A.b_bytes + 2048;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(conv3_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
-    cudaFuncSetAttribute(conv3_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
-    attr_set = true;
-  }
+  conv3_smem_attr();
   MDP_REQUIRE(smem <= 227 * 1024, "tc conv needs %zu bytes of shared memory", smem);
   int grid = A.ntiles < sm_count() ? A.ntiles : sm_count();
   if (zp == 4)
-    ::mdp::launch_k(conv3_tc_kernel<4>, grid, 256, smem, st, map, wmap, A);
+    ::mdp::launch_k(conv3_tc_kernel<4>, grid, 384, smem, st, map, wmap, A);
   else
-    ::mdp::launch_k(conv3_tc_kernel<2>, grid, 256, smem, st, map, wmap, A);
+    ::mdp::launch_k(conv3_tc_kernel<2>, grid, 384, smem, st, map, wmap, A);
   MDP_LAUNCH_CHECK("conv3_tc_kernel");
   if (A.ksplit > 1 && epi == EPI_HEAD) {
     const int64_t total = (int64_t)nb * S * S * S;
@@ -934,6 +1043,67 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
                                                  out_cq, out_q0);
     MDP_LAUNCH_CHECK("conv_split_reduce_kernel");
   }
+  return MDP_OK;
+}
+
+// enc1a on tensor cores (wide grids): xin = x-shifted input quads (pack_input_kernel mode 1),
+// w = the raw [16][2][27] filter; output 16 channels, bias, ReLU, TF32 rounding.
+int tc_enc1a(int nb, int S, const float4* xin, const float* w, const float* bias, float4* out, int out_cq,
+             int out_q0, cudaStream_t st) {
+  using namespace tc;
+  EncodeTiledFn enc = encode_fn();
+  MDP_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+  ConvArgs A{};
+  A.nb = nb;
+  A.S = S;
+  A.cin = 4;
+  A.cout = A.ncol = 16;
+  A.cqc = 1;
+  A.nchunk = A.cps = 1;
+  A.nsplit = A.ksplit = 1;
+  A.tx = ceil_div(S, BX);
+  A.ty = ceil_div(S, BY);
+  A.fold = 1;
+  A.pair = 1;
+  A.wraw = w;
+  // brick depth from the per-item shape only (batched == serial bitwise)
+  const int zp = (int64_t)A.tx * A.ty * ceil_div(S, 4) >= 2 * sm_count() ? 4 : 2;
+  A.tz = ceil_div(S, zp);
+  A.ntiles = nb * A.tx * A.ty * A.tz;
+  A.in_cq = 1;
+  A.in_q0 = 0;
+  A.bias = bias;
+  A.relu = 1;
+  A.epi = EPI_STORE;
+  A.out = out;
+  A.out_cq = out_cq;
+  A.out_q0 = out_q0;
+  A.Sout = S;
+  A.a_bytes = (uint32_t)(zp == 4 ? Brick<4>::QUAD_BYTES : Brick<2>::QUAD_BYTES);
+  A.na = 4;
+  A.resident = 1;
+  A.tps = 3;
+  A.nbs = 1;
+  A.b_bytes = 3 * 2 * 3 * 16 * 16;
+  A.tmem_cols = 128;  // 2 buffers x 4 planes x 16 columns
+  CUtensorMap map, wmap;
+  memset(&wmap, 0, sizeof(wmap));
+  cuuint64_t gdim[4] = {(cuuint64_t)4 * S, (cuuint64_t)S, (cuuint64_t)S, (cuuint64_t)nb};
+  cuuint64_t gstride[3] = {(cuuint64_t)16 * S, (cuuint64_t)16 * S * S, (cuuint64_t)16 * S * S * S};
+  cuuint32_t box[4] = {4 * HX, HY, (cuuint32_t)(zp + 2), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)xin, gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MDP_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d) for enc1a S=%d", (int)r, S);
+  const size_t smem = 1024 + (size_t)A.na * A.a_bytes + A.b_bytes + 2048;
+  conv3_smem_attr();
+  int grid = A.ntiles < sm_count() ? A.ntiles : sm_count();
+  if (zp == 4)
+    ::mdp::launch_k(conv3_tc_kernel<4>, grid, 384, smem, st, map, wmap, A);
+  else
+    ::mdp::launch_k(conv3_tc_kernel<2>, grid, 384, smem, st, map, wmap, A);
+  MDP_LAUNCH_CHECK("conv3_tc_kernel (enc1a)");
   return MDP_OK;
 }
 
