@@ -71,9 +71,10 @@ typedef struct mdp_problem {
   const double* p_val;
   const double* diag_c;    /* [nsys*ld] diag(C) for Jacobi (or NULL)        */
   int32_t qmax, umax, r1max, pad1; /* per-system maxima (launch shapes)      */
-  /* optional ELL copy of the pull list: entries of touched node u at
-   * [u*ell_w, (u+1)*ell_w), padded with value 0 (no row-pointer load on the
-   * pull's dependent-load chain); NULL: use u_ptr / u_q / u_val */
+  /* optional ELL copy of the head of the pull list: the first ell_w entries of
+   * touched node u at [u*ell_w, (u+1)*ell_w), padded with value 0 (no
+   * row-pointer load on the pull's dependent-load chain); entries beyond
+   * ell_w are read from u_ptr / u_q / u_val.  NULL: use only u_ptr / u_q / u_val */
   const int32_t* ell_q;
   const double* ell_val;
   int32_t ell_w, pad2;

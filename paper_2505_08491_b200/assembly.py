@@ -444,14 +444,13 @@ class DeviceProblem:
             k_val.append(K.data)
             PT = psi.T.tocsr()
             PT.sort_indices()
-            for row in range(s.n1):
-                if row in s.dirichlet_nodes:
-                    p_ptr.append(p_ptr[-1])
-                    continue
-                a, b = PT.indptr[row], PT.indptr[row + 1]
-                p_q.append(PT.indices[a:b].astype(np.int32) + q0)
-                p_val.append(PT.data[a:b])
-                p_ptr.append(p_ptr[-1] + (b - a))
+            # Psi^T rows of the free 1D nodes (Dirichlet rows stay empty), in row order
+            cnt_p = np.diff(PT.indptr)
+            cnt_p[np.asarray(s.dirichlet_nodes, dtype=np.int64)] = 0
+            src_p = _ranges(PT.indptr[:-1], cnt_p)
+            p_q.append(PT.indices[src_p].astype(np.int32) + q0)
+            p_val.append(PT.data[src_p])
+            p_ptr.extend((p_ptr[-1] + np.cumsum(cnt_p)).tolist())
             r1_start.append(r1_start[-1] + s.n1)
             diag[si, :self.n3] = diag_reduced(s)
             diag[si, self.n3:] = 1.0
@@ -470,7 +469,14 @@ class DeviceProblem:
         uq = np.concatenate(u_q) if u_q else np.zeros(0, dtype=np.int32)
         uv = np.concatenate(u_val) if u_val else np.zeros(0)
         cnt = np.diff(up)
-        ell_w = int(max(8, -(-int(cnt.max()) // 8) * 8)) if len(cnt) else 8
+        # width: the widest multiple of 8 whose padded table stays within 2x the list itself (ring-averaged
+        # Pi at 129^3: 5.4 entries per touched node on average but up to 44, so a full-width table would
+        # move 9x the bytes); wider rows continue in the CSR list (same per-lane summation order)
+        ell_w = 8
+        if len(cnt):
+            wmax = -(-int(cnt.max()) // 8) * 8
+            while ell_w + 8 <= wmax and len(cnt) * (ell_w + 8) <= 2 * int(cnt.sum()):
+                ell_w += 8
         nu = len(cnt)
         ell_q = np.zeros((max(nu, 1), ell_w), dtype=np.int32)
         ell_v = np.zeros((max(nu, 1), ell_w))
@@ -478,8 +484,9 @@ class DeviceProblem:
             pos = np.arange(len(uq)) - np.repeat(up[:-1], cnt)
             row = np.repeat(np.arange(nu), cnt)
             ell_q[:] = uq[up[:-1]][:, None]
-            ell_q[row, pos] = uq
-            ell_v[row, pos] = uv
+            head = pos < ell_w
+            ell_q[row[head], pos[head]] = uq[head]
+            ell_v[row[head], pos[head]] = uv[head]
         self._t = dict(
             wc=f64([s.params.coupling_weight for s in systems]), n1=i32(self.n1),
             q_start=i32(q_start), t_ptr=i32(t_ptr), t_col=i32(t_col), t_val=f64(t_val),

@@ -548,6 +548,8 @@ __device__ __forceinline__ void pull_rows(const mdp_problem& P, int s, int g0, i
       if (P.ell_q) {  // fixed-width rows: the entry loads depend on u only
         const int64_t b = (int64_t)u * P.ell_w;
         for (int k = sub; k < P.ell_w; k += 8) acc += P.ell_val[b + k] * sv[P.ell_q[b + k]];
+        // rows wider than the table continue in the CSR list (lane = entry index mod 8 either way)
+        for (int k = P.u_ptr[u] + P.ell_w + sub; k < P.u_ptr[u + 1]; k += 8) acc += P.u_val[k] * sv[P.u_q[k]];
       } else {
         for (int k = P.u_ptr[u] + sub; k < P.u_ptr[u + 1]; k += 8) acc += P.u_val[k] * sv[P.u_q[k]];
       }
