@@ -279,12 +279,28 @@ __device__ __forceinline__ StencilCoef stencil_coef(const Line1D& c, double kO, 
 // never holds non-finite garbage.
 constexpr int kSt3 = 6;  // stages; equals the unroll so slots are compile-time
 
+// Optional trace of three stencil blocks (first / middle / last slot) of the launch (build with
+// -DST3_TRACE; tools/stencil_trace.py): %globaltimer at block entry and after the ring is set up,
+// then per plane step the clock64 at which consumer warp 0 saw the stage full and finished the step.
+#ifdef ST3_TRACE
+__device__ long long g_st3_trace[3 * 64];
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define ST3_TR(which, k) \
+  do { if ((which) >= 0 && threadIdx.x == 0) g_st3_trace[(which) * 64 + (k)] = ((k) == 0 || (k) == 3) ? gtimer() : clock64(); } while (0)
+#else
+#define ST3_TR(which, k) do { } while (0)
+#endif
+
 template <int N, int RY, bool JAC, bool DIR, bool EDGE>
 __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* __restrict__ yp,
                                                   const double* __restrict__ jrp, const double* __restrict__ dgp,
                                                   double omega, int n, int i, int j, int z0, int z1,
                                                   const StencilCoef& K, const double* stg, int sw, int swj,
-                                                  uint64_t* full, uint64_t* empty, int r_lo, int r_hi) {
+                                                  uint64_t* full, uint64_t* empty, int r_lo, int r_hi, int trc) {
   using namespace async;
   constexpr int NR = RY + 2;
   const int lane = threadIdx.x & 31;
@@ -292,6 +308,8 @@ __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* 
   const bool col_in = i < n;
   const int ic = col_in ? i : n - 1;  // clamped column (reads stay inside the stage)
   // neighbour masks: absent (outside) or eliminated (Dirichlet face) columns contribute 0
+  // (as 0/1 factors: selects instead of the two FP64 operations measured 6-10% slower per step --
+  // the step is a latency chain, not FP64-issue bound)
   const double mL = (ic - 1 >= (DIR ? 1 : 0)) ? 1.0 : 0.0;
   const double mR = (ic + 1 <= (DIR ? n - 2 : n - 1)) ? 1.0 : 0.0;
   int roff[NR];
@@ -327,6 +345,7 @@ __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* 
       const int kc = k < 0 ? 0 : (k > n - 1 ? n - 1 : k);  // plane the producer copied
       const bool pok = k >= 0 && k < n && !(DIR && (k == 0 || k == n - 1));
       mbar_wait(&full[u], par);
+      if (st < 24) ST3_TR(trc, 4 + 2 * st);
       const double* b = stg + (size_t)u * (sw + 2 * swj) + ((kc * nn + r_lo * n) & 1);
       double c[NR], lr[NR];
 #pragma unroll
@@ -394,8 +413,10 @@ __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* 
         Un[r] = un;
         Cn[r] = cn;
       }
+      if (st < 24) ST3_TR(trc, 5 + 2 * st);
     }
   }
+  ST3_TR(trc, 3);
 }
 
 #ifndef STENCIL3_MINB
@@ -438,6 +459,15 @@ __global__ void __launch_bounds__(256, STENCIL3_MINB) stencil3_kernel(const mdp_
   const int z1 = min(n, z0 + zchunk);
   if (j >= n || z0 >= n) return;  // gather-slice width / chunk rounding
   const bool dir = P.bc3d != 0;
+  int trc = -1;
+#ifdef ST3_TRACE
+  {
+    const int nslots = gridDim.x - gx;
+    trc = blockIdx.y != 0 ? -1 : (slot == 0 ? 0 : (slot == nslots / 2 ? 1 : (slot == nslots - 1 ? 2 : -1)));
+    ST3_TR(trc, 0);
+    ST3_TR(trc, 2);
+  }
+#endif
   if (threadIdx.x == 0) {
     for (int t = 0; t < kSt3; ++t) {
       mbar_init(&full[t], 1);
@@ -450,6 +480,7 @@ __global__ void __launch_bounds__(256, STENCIL3_MINB) stencil3_kernel(const mdp_
   for (int t = threadIdx.x; t < kSt3 * sws + 2; t += blockDim.x) stg[t - 2] = 0.0;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes before the async-proxy copies
   __syncthreads();
+  ST3_TR(trc, 1);
   const double* xp = x + (int64_t)s * ldx;
   const int r_lo = j - 1 < 0 ? 0 : j - 1;
   const int r_hi = j + RY > n - 1 ? n - 1 : j + RY;
@@ -496,7 +527,7 @@ __global__ void __launch_bounds__(256, STENCIL3_MINB) stencil3_kernel(const mdp_
   const int lo = dir ? 1 : 0, hi = dir ? n - 2 : n - 1;
   const bool edge = (j - 1 < lo) || (j + RY > hi);
 #define MDP_ST3(D, E) \
-  stencil3_consumer<N, RY, JAC, D, E>(P, yp, jrp, dgp, omega, n, i, j, z0, z1, K, stg, sw, swj, full, empty, r_lo, r_hi)
+  stencil3_consumer<N, RY, JAC, D, E>(P, yp, jrp, dgp, omega, n, i, j, z0, z1, K, stg, sw, swj, full, empty, r_lo, r_hi, trc)
   if (dir) {
     if (edge) MDP_ST3(true, true); else MDP_ST3(true, false);
   } else {
@@ -668,21 +699,46 @@ static int env_int(const char* name, int dflt) {
 }
 
 template <int N, int RY>
-static void launch_stencil3_t(dim3 grid, int threads, size_t smem, cudaStream_t st, const mdp_problem* p,
-                              const int32_t* sel, const double* x, int64_t ldx, double* y, int64_t ldy, int zchunk,
-                              const double* jr, double omega, const GatherArgs& G) {
+static void launch_stencil3_attr() {
   static bool attr = false;  // opt in to > 48 KB dynamic shared memory once per instantiation
   if (!attr) {
     cudaFuncSetAttribute(stencil3_kernel<N, RY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(stencil3_kernel<N, RY, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
+}
+
+template <int N, int RY>
+static void launch_stencil3_t(dim3 grid, int threads, size_t smem, cudaStream_t st, const mdp_problem* p,
+                              const int32_t* sel, const double* x, int64_t ldx, double* y, int64_t ldy, int zchunk,
+                              const double* jr, double omega, const GatherArgs& G) {
+  launch_stencil3_attr<N, RY>();
   if (jr)
     ::mdp::launch_k(stencil3_kernel<N, RY, true>, grid, threads, smem, st, *p, sel, x, ldx, y, ldy, zchunk, jr, omega,
                     G);
   else
     ::mdp::launch_k(stencil3_kernel<N, RY, false>, grid, threads, smem, st, *p, sel, x, ldx, y, ldy, zchunk, jr,
                     omega, G);
+}
+
+// resident blocks per SM of one instantiation at this launch shape (registers AND shared memory;
+// the 156-register consumer holds 129^3 to 2 blocks of 192 threads per SM, not the 5 its ring would allow)
+template <int N, int RY>
+static int stencil3_blocks_per_sm(int threads, size_t smem, bool jac, int n) {
+  static int cache[2][2] = {{0, 0}, {0, 0}};  // [jac] -> (n, blocks)
+  int* c = cache[jac ? 1 : 0];
+  if (c[0] == n && c[1] > 0) return c[1];
+  launch_stencil3_attr<N, RY>();
+  int nb = 0;
+  cudaError_t e = jac ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, stencil3_kernel<N, RY, true>, threads, smem)
+                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, stencil3_kernel<N, RY, false>, threads, smem);
+  if (e != cudaSuccess || nb < 1) {
+    cudaGetLastError();
+    nb = 1;
+  }
+  c[0] = n;
+  c[1] = nb;
+  return nb;
 }
 
 // v3 launch: one block per (RY-row band, z-chunk, system): tiles_x consumer
@@ -701,15 +757,45 @@ static int launch_stencil3(const mdp_problem* p, int32_t nsel, const int32_t* se
   const size_t swj = jr ? (size_t)((RY * n + 3) & ~1) : 0;  // Jacobi: r and diag(C) bands ride in the stage
   const size_t smem = 16 * (size_t)S + (size_t)S * (sw + 2 * swj) * 8 + 32;
   MDP_REQUIRE(smem <= 200 * 1024, "stencil stage ring of %zu bytes exceeds shared memory (n = %d, RY = %d)", smem, n, RY);
-  // z-chunks: ~4 waves of blocks (occupancy from shared memory, <= 8 blocks/SM)
-  int per_sm = (int)((200 * 1024) / smem);
-  per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
-  static const int waves = env_int("MDP_STENCIL_WAVES", 4);
-  const int64_t want = (int64_t)waves * per_sm * sm_count();
-  int zch = ceil_div(want, (int64_t)bands * nsel);
+  // z-chunks.  A block's life is a serial chain: ring set-up + the first DRAM round trip (~3.5 plane
+  // steps' worth, traced) and then one step per plane of its chunk plus 2 halo planes; blocks run in waves
+  // of (resident blocks per SM) x SMs.  Pick the chunk count that minimises waves x chain length.
+  int per_sm = 1;
+#define MDP_ST3O(NN, R) per_sm = stencil3_blocks_per_sm<NN, R>(threads, smem, jr != nullptr, n)
+  if (RY == 2) {
+    switch (n) {
+      case 17: MDP_ST3O(17, 2); break;
+      case 33: MDP_ST3O(33, 2); break;
+      default: MDP_ST3O(0, 2); break;
+    }
+  } else if (RY == 8) {
+    MDP_ST3O(0, 8);
+  } else {
+    switch (n) {
+      case 65: MDP_ST3O(65, 4); break;
+      case 129: MDP_ST3O(129, 4); break;
+      case 193: MDP_ST3O(193, 4); break;
+      default: MDP_ST3O(0, 4); break;
+    }
+  }
+#undef MDP_ST3O
+  const int64_t slots = (int64_t)per_sm * sm_count();
   const int minlen = n <= 48 ? 2 : 8;
   const int zmax = n / minlen > 1 ? n / minlen : 1;
-  zch = zch < 1 ? 1 : (zch > zmax ? zmax : zch);
+  int zch = 1;
+  double best = 1e300;
+  for (int c = 1; c <= zmax; ++c) {
+    const int len = ceil_div(n, c);
+    // chunks beyond ~40 planes lose in the coupled / Jacobi launches (few long blocks: the dependent
+    // phase-2 launch waits on the slowest; profiles/r02_stencil_stream.txt)
+    if (len > 40 && c < zmax) continue;
+    const int64_t blocks = (int64_t)bands * ceil_div(n, len) * nsel;
+    const double cost = (double)ceil_div(blocks, slots) * (3.5 + len + 2);
+    if (cost < best - 1e-9) {
+      best = cost;
+      zch = c;
+    }
+  }
   int zchunk = ceil_div(n, zch);
   static const int forced = env_int("MDP_STENCIL_ZCHUNK", 0);
   if (forced > 0) zchunk = forced < n ? forced : n;
@@ -917,3 +1003,9 @@ extern "C" int mdp_jacobi_sweep(const mdp_problem* p, int32_t nsel, const int32_
   MDP_LAUNCH_CHECK("jacobi_update_kernel");
   return MDP_OK;
 }
+
+#ifdef ST3_TRACE
+extern "C" int mdp_st3_trace_read(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, mdp::g_st3_trace, sizeof(long long) * 3 * 64);
+}
+#endif
