@@ -910,6 +910,22 @@ static int validate(const mdp_problem* p, int32_t nsel) {
   return MDP_OK;
 }
 
+// Stencil launch + the Pi gather s = W (T x3 - Psi D x1).  Small grids: the gather rides in the
+// stencil launch (first blocks; one launch fewer on a latency-bound step).  Wide grids: gather blocks
+// inside the stencil launch inherit its footprint (150 registers, a stage ring: 2 blocks per SM), so
+// their dependent-load chains hold stencil slots at 12 warps per SM; for batches of wide grids the
+// gather is its own launch of light blocks ahead of the stencil (129^3 x 64 coupled SpMV 594 -> 513 us,
+// 65^3 x 16 52 -> 44 us; one 129^3 system is 1 us faster folded; MDP_GATHER_MODE=0/1 forces either).
+static int stencil_and_gather(const mdp_problem* p, int32_t nsel, const int32_t* sel, const double* x, int64_t ldx,
+                              double* y, int64_t ldy, cudaStream_t st, const double* jr, double omega,
+                              const GatherArgs& g) {
+  static const int mode = env_int("MDP_GATHER_MODE", -1);
+  const bool separate = mode >= 0 ? mode == 1 : (p->n >= 65 && nsel >= 4);
+  if (!separate) return launch_stencil(p, nsel, sel, x, ldx, y, ldy, st, jr, omega, &g);
+  if (int rc = launch_gather(p, nsel, sel, g.x3, g.x1, ldx, g.s_out, st)) return rc;
+  return launch_stencil(p, nsel, sel, x, ldx, y, ldy, st, jr, omega, nullptr);
+}
+
 }  // namespace mdp
 
 using namespace mdp;
@@ -965,7 +981,7 @@ extern "C" int mdp_coupled_spmv(const mdp_problem* p, int32_t nsel, const int32_
   // launch 2: y3 += w T^T s and y1 = K11 x1 - w D Psi^T s
   GatherArgs g{x, x + n3, s_work};
   int rc;
-  if ((rc = launch_stencil(p, nsel, sel, x, p->ld, y, p->ld, st, nullptr, 0.0, &g))) return rc;
+  if ((rc = stencil_and_gather(p, nsel, sel, x, p->ld, y, p->ld, st, nullptr, 0.0, g))) return rc;
   return launch_phase2(p, nsel, sel, s_work, 1.0, y, p->ld, st, nullptr, x + n3, y + n3);
 }
 
@@ -976,7 +992,7 @@ extern "C" int mdp_reduced_spmv(const mdp_problem* p, int32_t nsel, const int32_
   cudaStream_t st = (cudaStream_t)stream;
   GatherArgs g{x3, nullptr, s_work};
   int rc;
-  if ((rc = launch_stencil(p, nsel, sel, x3, p->ld, y3, p->ld, st, nullptr, 0.0, &g))) return rc;
+  if ((rc = stencil_and_gather(p, nsel, sel, x3, p->ld, y3, p->ld, st, nullptr, 0.0, g))) return rc;
   return launch_phase2(p, nsel, sel, s_work, 1.0, y3, p->ld, st, nullptr, nullptr, nullptr);
 }
 
@@ -992,7 +1008,7 @@ extern "C" int mdp_jacobi_sweep(const mdp_problem* p, int32_t nsel, const int32_
     // epilogue; then out -= omega w (T^T s) / d at the touched nodes
     GatherArgs g{x, nullptr, s_work};
     int rc;
-    if ((rc = launch_stencil(p, nsel, sel, x, p->ld, x_out, p->ld, st, r, omega, &g))) return rc;
+    if ((rc = stencil_and_gather(p, nsel, sel, x, p->ld, x_out, p->ld, st, r, omega, g))) return rc;
     return launch_phase2(p, nsel, sel, s_work, -omega, x_out, p->ld, st, p->diag_c, nullptr, nullptr);
   }
   (void)tmp;
