@@ -575,6 +575,15 @@ __device__ __forceinline__ void pull_rows(const mdp_problem& P, int s, int g0, i
     const int u = P.u_start[s] + base;
     const bool live = base < ucount;
     double acc = 0.0;
+    // the read-modify-write operand (and the divisor) are fetched ahead of the entry loads: their
+    // DRAM round trip overlaps the list's instead of following the reduction
+    int64_t g = 0;
+    double yv = 0.0, dv = 1.0;
+    if (live && sub == 0) {
+      g = (int64_t)s * ld + P.u_node[u];
+      yv = y3[g];
+      if (div) dv = div[g];
+    }
     if (live)
       if (P.ell_q) {  // fixed-width rows: the entry loads depend on u only
         const int64_t b = (int64_t)u * P.ell_w;
@@ -587,11 +596,10 @@ __device__ __forceinline__ void pull_rows(const mdp_problem& P, int s, int g0, i
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (live && sub == 0) {
-      const int64_t g = (int64_t)s * ld + P.u_node[u];
       if (div)
-        y3[g] -= (-alpha * (P.wc[s] * acc)) / div[g];
+        y3[g] = yv - (-alpha * (P.wc[s] * acc)) / dv;
       else
-        y3[g] += alpha * P.wc[s] * acc;
+        y3[g] = yv + alpha * P.wc[s] * acc;
     }
   }
 }
