@@ -113,8 +113,11 @@ def test_unet_forward_vs_reference(gpu, path, tol):
     assert rel(yb, g["yb"]) <= tol
 
 
-@pytest.mark.parametrize("n", [33, 65])
+@pytest.mark.parametrize("n", [33, 65, 70])
 def test_unet_forward_large_vs_oracle(gpu, n):
+    """33: CUDA-core enc1a, split-N / split-K layers; 65 and 70: tensor-core enc1a (n >= 64) with bricks
+    cut by every face (70 = 8 * 8 + 6 = 16 * 4 + 6 = 4 * 17 + 2), 4-plane bricks; 70 also takes the
+    transposed convs with output padding 0 and 1 (m = 35, q = 17)."""
     import oracle
     from paper_2505_08491_b200 import neural
     rng = np.random.default_rng(n)

@@ -4,8 +4,10 @@ Grids n in {33, 65, 129, 193} x batch {1, 8, 64} of seeded 32-segment trees.
 Timed separately (CUDA events, L2 flushed -- written, then read back -- before
 every timed rep): the K00 stencil alone, the coupled block SpMV, Pi gather, Pi^T scatter (pull), 30-vector Arnoldi
 orthogonalisation, and the CNN preconditioner forward.  Algorithmic bytes /
-FLOPs per SURVEY.md section 8d; peaks from MEASURED_PEAKS.json (HBM) and a
-cuBLAS TF32 GEMM measured in the same run.
+FLOPs per SURVEY.md section 8d; peaks from MEASURED_PEAKS.json (HBM; TF32 = bf16 / 2, the
+cuBLAS TF32 GEMM rate of the same run is recorded beside it).  The stencil and the coupled SpMV
+are also timed streamed over rotating vector pairs; the gather / scatter rows carry the
+launch + event floor of the timing method (a 1-element kernel).
 
     python tools/bench_ops.py [--sizes 33,65,129,193] [--batches 1,8,64] [--out f.json]
                               [--cpu-sizes 33,65,129] [--cpu-cnn-max 65]
@@ -51,8 +53,11 @@ def main():
     a = ap.parse_args()
     lib = _ext.lib()
     pk = bench.peaks()
-    tf32 = bench.measure_tf32_peak()
+    cublas_tf32 = bench.measure_tf32_peak()
+    tf32 = pk["bf16_tflops"] / 2  # kind::tf32 = half the dense bf16 rate (MEASURED_PEAKS); cuBLAS TF32 is a note
     flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device="cuda")
+    one = torch.zeros(1, device="cuda")
+    floor_ms = bench.device_ms(lambda: one.add_(1.0), 10, flush=flush, hide_us=2000)  # launch + event floor
     from paper_2505_08491_b200.assembly import DeviceProblem
     from paper_2505_08491_b200.operators import CoupledOperator, CouplingOps
     rows = []
@@ -85,13 +90,23 @@ def main():
             byt = sum(16 * x for x in N) + 40 * Q
             r["spmv"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9, "frac_hbm": byt / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
                          "frac_hbm_spec_8tbs": byt / (ms * 1e-3) / 8e12, "bytes": byt}
+            # the same launches streamed over rotating vector pairs (> 2x L2 in total), back to back
+            nset = min(16, max(2, int(-(-2.5 * 126e6 // byt))))
+            if nset * 2 * nb * prob.ld * 8 < 40e9:
+                XS = [prob.zeros().normal_() for _ in range(nset)]
+                YS = [prob.zeros() for _ in range(nset)]
+                for key, fn in (("stencil", ops.stencil), ("spmv", A.matvec)):
+                    sms = bench.device_ms_stream([(lambda X_=X_, Y_=Y_, fn=fn: fn(X_, Y_)) for X_, Y_ in zip(XS, YS)], 3)
+                    r[key]["stream_ms"] = sms
+                    r[key]["stream_frac_hbm"] = r[key]["bytes"] / (sms * 1e-3) / 1e9 / pk["hbm_gbs"]
+                del XS, YS
             S = torch.zeros(max(Q, 1), dtype=torch.float64, device="cuda")
             ms = timed(lambda: ops.gather(X, None, S), a.reps, flush)
             byt = 112 * Q
-            r["pi_gather"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9, "bytes": byt}
+            r["pi_gather"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9, "bytes": byt, "launch_floor_ms": floor_ms}
             ms = timed(lambda: ops.scatter(S, 1.0, Y), a.reps, flush)
             byt = 48 * Q + 16 * U
-            r["pi_scatter"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9, "bytes": byt}
+            r["pi_scatter"] = {"ms": ms, "GBps": byt / (ms * 1e-3) / 1e9, "bytes": byt, "launch_floor_ms": floor_ms}
             # Arnoldi: 30 basis vectors (k = 30), orthogonalise w against all of them
             k = 30
             nmax = max(N)
@@ -130,7 +145,8 @@ def main():
             del prob, A, ops, X, Y, S, D, Z, R
             torch.cuda.empty_cache()
     cpu = [cpu_row(int(n), a.cpu_cnn_max) for n in a.cpu_sizes.split(",") if n]
-    out = {"peaks": pk, "tf32_tflops_measured": tf32, "rows": rows, "cpu_oracle": cpu}
+    out = {"peaks": pk, "tf32_peak_used": tf32, "cublas_tf32_tflops_this_run": cublas_tf32, "launch_floor_ms": floor_ms,
+           "rows": rows, "cpu_oracle": cpu}
     if a.out:
         Path(a.out).write_text(json.dumps(out, indent=1))
 
