@@ -798,6 +798,35 @@ __global__ void __launch_bounds__(192, 1) tconv_tc_kernel(const TconvArgs T) {
       mbar_wait(&tfull[buf], (it >> 1) & 1);
       fence_after();
       const uint32_t d0 = tmem + lane_addr + (uint32_t)buf * tstride;
+      if (T.tg >= 2) {
+        // taps t, t + 1 differ in a only: output voxels 2x and 2x + 1 are the two 16-byte halves of
+        // one 32-byte run, written back to back so L2 sees both halves of a sector together
+        for (int t = 0; t < T.tg; t += 2) {
+          const int tap = grp * T.tg + t;
+          const int64_t o = ((int64_t)(2 * z + (tap >> 2)) * So + 2 * y + ((tap >> 1) & 1)) * So + 2 * x;
+          for (int cg = 0; cg < T.cout / 16; ++cg) {
+            float r0[16], r1[16];
+            tmem_ld16(d0 + (uint32_t)(t * T.cout + cg * 16), r0);
+            tmem_ld16(d0 + (uint32_t)((t + 1) * T.cout + cg * 16), r1);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float bi = T.bias ? T.bias[cg * 16 + i] : 0.f;
+              r0[i] = tf32_round(fmaxf(r0[i] + bi, 0.f));
+              r1[i] = tf32_round(fmaxf(r1[i] + bi, 0.f));
+            }
+            if (live)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                float4* dst = T.out + ((int64_t)b * T.out_cq + T.out_q0 + cg * 4 + q) * nvo + o;
+                dst[0] = make_float4(r0[4 * q], r0[4 * q + 1], r0[4 * q + 2], r0[4 * q + 3]);
+                dst[1] = make_float4(r1[4 * q], r1[4 * q + 1], r1[4 * q + 2], r1[4 * q + 3]);
+              }
+          }
+        }
+        fence_before();
+        mbar_arrive(&tempty[buf]);
+        continue;
+      }
       for (int t = 0; t < T.tg; ++t) {
         const int tap = grp * T.tg + t;
         const int64_t o = ((int64_t)(2 * z + (tap >> 2)) * So + 2 * y + ((tap >> 1) & 1)) * So + 2 * x + (tap & 1);
