@@ -422,8 +422,12 @@ __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* 
 #ifndef STENCIL3_MINB
 #define STENCIL3_MINB 1  // lifts the compiler's 128-register choice (129^3 x 8: 2.8 -> 3.6 TB/s)
 #endif
+// 193^3 runs 8 warps per block: at 150 registers only ONE block fits an SM, at 128 (a few bytes of
+// spills) two do: K00 stencil 193^3 x 8 0.72 -> 0.86 of HBM, coupled SpMV 0.63 -> 0.74 (the Jacobi
+// variant spills ~400 B at 128 and loses, so it keeps its registers).  The 6-warp blocks of 129^3 already hold
+// two; squeezing a third in (112 registers) costs more in spills than the occupancy returns.
 template <int N, int RY, bool JAC>
-__global__ void __launch_bounds__(256, STENCIL3_MINB) stencil3_kernel(const mdp_problem P, const int32_t* sel,
+__global__ void __launch_bounds__(256, (N > 160 && N <= 224 && !JAC) ? 2 : STENCIL3_MINB) stencil3_kernel(const mdp_problem P, const int32_t* sel,
                                                         const double* __restrict__ x, int64_t ldx,
                                                         double* __restrict__ y, int64_t ldy, int zchunk,
                                                         const double* __restrict__ jr, double omega,
