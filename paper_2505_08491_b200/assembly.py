@@ -337,20 +337,50 @@ def host_reduced_operator(system: CoupledSystem) -> sp.csr_matrix:
     return (system.K00 + system.params.coupling_weight * system.M00).tocsr()
 
 
-def diag_reduced(system: CoupledSystem) -> np.ndarray:
-    """diag(C) = diag(K00) + w diag(M00) without assembling K00 (Kronecker diagonal)."""
-    n, h, p = system.grid.n, system.grid.h, system.params
+def diag_k00(grid, params, bc3d: str) -> np.ndarray:
+    """diag(K00) from the Kronecker factors (no assembly); eliminated cube nodes carry 1."""
+    n, h = grid.n, grid.h
     idx = np.arange(n)
     end = (idx == 0) | (idx == n - 1)
     k1 = np.where(end, 1.0 / h, 2.0 / h)
     m1 = np.where(end, 2.0 * h / 6.0, 4.0 * h / 6.0)
     kz, ky, kx = np.meshgrid(k1, k1, k1, indexing="ij")
     mz, my, mx = np.meshgrid(m1, m1, m1, indexing="ij")
-    d = (p.k_omega * (mz * my * kx + mz * ky * mx + kz * my * mx) + p.sigma_omega * (mz * my * mx)).ravel()
-    T = system.restriction.matrix
-    d = d + p.coupling_weight * np.asarray(T.multiply(T).T @ system.restriction.weights).ravel()
-    if system.bc3d == "dirichlet":
+    d = (params.k_omega * (mz * my * kx + mz * ky * mx + kz * my * mx) + params.sigma_omega * (mz * my * mx)).ravel()
+    if bc3d == "dirichlet":
         d[cube_boundary_mask(n)] = 1.0
+    return d
+
+
+def _by_node(T) -> tuple:
+    """Stored entries of T grouped by 3D node, quadrature rows ascending within a node (the order of
+    T.T.tocsr()), without any O(N3) work: (touched nodes, group starts, group sizes, entry order, rows)."""
+    T = T.tocsr()
+    T.sort_indices()
+    rows = np.repeat(np.arange(T.shape[0]), np.diff(T.indptr))
+    order = np.argsort(T.indices, kind="stable")
+    nodes, start, cnt = np.unique(T.indices[order], return_index=True, return_counts=True)
+    return nodes.astype(np.int64), start, cnt, order, rows, T
+
+
+def diag_m00(system: CoupledSystem, by_node=None) -> tuple:
+    """Nonzeros of w diag(M00) = w (T o T)^T W: (free node ids, values); per node the terms are summed
+    in ascending quadrature order, as the sparse product does."""
+    nodes, start, cnt, order, rows, T = by_node or _by_node(system.restriction.matrix)
+    terms = (T.data[order] * T.data[order]) * system.restriction.weights[rows[order]]
+    v = system.params.coupling_weight * np.bincount(np.repeat(np.arange(len(nodes)), cnt), weights=terms,
+                                                     minlength=len(nodes))
+    keep = v != 0.0
+    if system.bc3d == "dirichlet":
+        keep &= ~cube_boundary_mask(system.grid.n)[nodes]
+    return nodes[keep], v[keep]
+
+
+def diag_reduced(system: CoupledSystem) -> np.ndarray:
+    """diag(C) = diag(K00) + w diag(M00) without assembling K00 (Kronecker diagonal)."""
+    d = diag_k00(system.grid, system.params, system.bc3d)
+    nodes, vals = diag_m00(system)
+    d[nodes] = d[nodes] + vals
     return d
 
 
@@ -396,7 +426,10 @@ class DeviceProblem:
         q_start, t_ptr, t_col, t_val, psi_col, psi_val, wq = [0], [0], [], [], [], [], []
         u_start, u_node, u_ptr, u_q, u_val = [0], [], [0], [], []
         r1_start, k_ptr, k_col, k_val, p_ptr, p_q, p_val = [0], [0], [], [], [0], [], []
-        diag = np.zeros((self.nsys, self.ld))
+        # diag(C) per system = the shared diag(K00) (one upload for the whole batch) + w diag(M00) at the
+        # touched nodes; assembled on the device: at 129^3 x 64 the per-system host diagonals and their
+        # 1.1 GB upload were most of the set-up time
+        dnodes, dvals, dsys = [], [], []
         for si, s in enumerate(systems):
             T = s.restriction.matrix.tocsr()
             T.sort_indices()
@@ -423,16 +456,15 @@ class DeviceProblem:
             psi_val.append(psi.data)
             wq.append(s.restriction.weights)
             q_start.append(q0 + Q)
-            # pull rows: T^T over touched free nodes
-            TT = T.T.tocsr()
-            TT.sort_indices()
-            nz = np.nonzero(np.diff(TT.indptr))[0]
+            # pull rows: T^T over touched free nodes (entries grouped by node, no O(N3) pass)
+            bn = _by_node(T)
+            nz, st_u, cnt_u, order_u, rows_u, Ts = bn
             if bmask is not None:
-                nz = nz[~bmask[nz]]
-            cnt_u = TT.indptr[nz + 1] - TT.indptr[nz]
-            src = _ranges(TT.indptr[nz], cnt_u)
-            u_q.append(TT.indices[src].astype(np.int32) + q0)
-            u_val.append(TT.data[src])
+                free = ~bmask[nz]
+                nz, st_u, cnt_u = nz[free], st_u[free], cnt_u[free]
+            src = order_u[_ranges(st_u, cnt_u)]
+            u_q.append(rows_u[src].astype(np.int32) + q0)
+            u_val.append(Ts.data[src])
             u_ptr.extend((u_ptr[-1] + np.cumsum(cnt_u)).tolist())
             u_node.append(nz.astype(np.int32))
             u_start.append(u_start[-1] + len(nz))
@@ -452,8 +484,9 @@ class DeviceProblem:
             p_val.append(PT.data[src_p])
             p_ptr.extend((p_ptr[-1] + np.cumsum(cnt_p)).tolist())
             r1_start.append(r1_start[-1] + s.n1)
-            diag[si, :self.n3] = diag_reduced(s)
-            diag[si, self.n3:] = 1.0
+            nd, vd = diag_m00(s, bn)
+            dnodes.append(nd + si * self.ld)
+            dvals.append(vd)
 
         def i32(x):
             x = np.concatenate(x) if isinstance(x, list) and x and isinstance(x[0], np.ndarray) else np.asarray(x)
@@ -496,7 +529,7 @@ class DeviceProblem:
             r1_start=i32(r1_start), k_ptr=i32(k_ptr), k_col=i32(k_col), k_val=f64(k_val),
             p_ptr=i32(p_ptr), p_q=i32(p_q if p_q else [np.zeros(0)]),
             p_val=f64(p_val if p_val else [np.zeros(0)]),
-            diag_c=torch.as_tensor(diag, device=dev),
+            diag_c=self._device_diag(systems[0], bcs, dnodes, dvals, dev),
             ell_q=i32(ell_q), ell_val=f64(ell_v),
         )
         self.Qtot = int(q_start[-1])
@@ -515,6 +548,19 @@ class DeviceProblem:
         self.desc = P
         self.s_work = torch.zeros(max(1, self.Qtot), dtype=torch.float64, device=dev)
         self.ilu = None
+
+    def _device_diag(self, s0, bcs, dnodes, dvals, dev):
+        import torch
+        base = torch.ones(self.ld, dtype=torch.float64, device=dev)
+        base[:self.n3] = torch.as_tensor(diag_k00(s0.grid, s0.params, "dirichlet" if bcs == {"dirichlet"} else "neumann"),
+                                         device=dev)
+        D = base.repeat(self.nsys, 1)
+        if dnodes and sum(len(x) for x in dnodes):
+            idx = torch.as_tensor(np.concatenate(dnodes), device=dev)
+            val = torch.as_tensor(np.concatenate(dvals), device=dev)
+            flat = D.view(-1)
+            flat[idx] = flat[idx] + val  # each touched node appears once per system: plain gather / add / put
+        return D
 
     # -- host <-> device vector layout -------------------------------------------------
     def zeros(self):
