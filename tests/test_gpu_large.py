@@ -133,3 +133,22 @@ def test_cfg2_full_solve_outcome_vs_oracle(gpu, tmp_path):
     assert rep.converged == bool(g["conv"]) and rep.iterations == int(g["iters"])
     assert abs(rep.rel_residual / float(g["rel"]) - 1) <= 0.1, (rep.rel_residual, float(g["rel"]))
     assert np.allclose(rep.residual_history[:13], g["hist"][:13], rtol=5e-3)
+
+
+def test_cfg4_and_cfg3_solves_repeat_bitwise(gpu, tmp_path):
+    """Run-to-run determinism at the target sizes (stands in for racecheck, which this pool refuses):
+    the whole pipeline -- TMA / mbarrier rings, TMEM double buffering, fixed-partition reductions, the pull --
+    must reproduce the residual history and the solution bit for bit, for the single 129^3 system and for
+    the 16-system 65^3 batch, the second run going through freshly built solver objects."""
+    from paper_2505_08491_b200 import configs, harness
+    s4 = configs.cfg4().systems[0]
+    runs = [_head(s4, _spec(tmp_path, 3), 50, 1e-8, 6) for _ in range(2)]
+    assert runs[0][2].residual_history == runs[1][2].residual_history
+    assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
+    wl = configs.cfg3()
+    st = harness.CoupledStrategy(tol=1e-6, maxit=3, restart=50, inner_iterations=3, three_d=_spec(tmp_path, 2))
+    a = harness.solve_coupled(wl.systems, st)
+    b = harness.solve_coupled(wl.systems, st)
+    for (u3a, u1a, ra), (u3b, u1b, rb) in zip(a, b):
+        assert ra.residual_history == rb.residual_history
+        assert np.array_equal(u3a, u3b) and np.array_equal(u1a, u1b)
