@@ -572,6 +572,20 @@ __device__ __forceinline__ void pull_rows(const mdp_problem& P, int s, int g0, i
                                           int64_t ld, const double* __restrict__ div) {
   const int sub = threadIdx.x & 7;
   const int ucount = P.u_start[s + 1] - P.u_start[s];
+  // launch-invariant list data of this group's first node, fetched BEFORE the grid dependency wait (the
+  // kernel is launched as a programmatic dependent: its launch latency and this DRAM round trip overlap
+  // the stencil's tail); s and y3 are only touched after the wait
+  int q_first = 0, node_first = 0;
+  double v_first = 0.0;
+  if (g0 < ucount) {
+    const int u0 = P.u_start[s] + g0;
+    node_first = P.u_node[u0];
+    if (P.ell_q && sub < P.ell_w) {
+      q_first = P.ell_q[(int64_t)u0 * P.ell_w + sub];
+      v_first = P.ell_val[(int64_t)u0 * P.ell_w + sub];
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // the 8-lane groups of a warp iterate together (shuffles need all lanes)
   const int gfirst = g0 - ((threadIdx.x & 31) >> 3);
   for (int it = 0; gfirst + it * gstride < ucount; ++it) {
@@ -584,14 +598,19 @@ __device__ __forceinline__ void pull_rows(const mdp_problem& P, int s, int g0, i
     int64_t g = 0;
     double yv = 0.0, dv = 1.0;
     if (live && sub == 0) {
-      g = (int64_t)s * ld + P.u_node[u];
+      g = (int64_t)s * ld + (it == 0 ? node_first : P.u_node[u]);
       yv = y3[g];
       if (div) dv = div[g];
     }
     if (live)
       if (P.ell_q) {  // fixed-width rows: the entry loads depend on u only
         const int64_t b = (int64_t)u * P.ell_w;
-        for (int k = sub; k < P.ell_w; k += 8) acc += P.ell_val[b + k] * sv[P.ell_q[b + k]];
+        if (it == 0) {
+          if (sub < P.ell_w) acc += v_first * sv[q_first];
+          for (int k = sub + 8; k < P.ell_w; k += 8) acc += P.ell_val[b + k] * sv[P.ell_q[b + k]];
+        } else {
+          for (int k = sub; k < P.ell_w; k += 8) acc += P.ell_val[b + k] * sv[P.ell_q[b + k]];
+        }
         // rows wider than the table continue in the CSR list (lane = entry index mod 8 either way)
         for (int k = P.u_ptr[u] + P.ell_w + sub; k < P.u_ptr[u + 1]; k += 8) acc += P.u_val[k] * sv[P.u_q[k]];
       } else {
@@ -642,12 +661,13 @@ __global__ void __launch_bounds__(256) coupling_phase2_kernel(const mdp_problem 
                                                                const double* __restrict__ div,
                                                                const double* __restrict__ x1,
                                                                double* __restrict__ y1) {
-  MDP_PDL_ENTER();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int s = sys_of(sel, blockIdx.y);
   if ((int)blockIdx.x < bpull) {
     pull_rows(P, s, blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3), bpull * (blockDim.x >> 3), sv, alpha, y3,
-              ld, div);
+              ld, div);  // waits on the previous grid after its list prologue
   } else if (y1) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int b = blockIdx.x - bpull, nb = gridDim.x - bpull;
     oned_rows(P, s, b * (blockDim.x >> 2) + (threadIdx.x >> 2), nb * (blockDim.x >> 2), x1, sv, y1, ld);
   }
@@ -909,7 +929,11 @@ static int launch_phase2(const mdp_problem* p, int32_t nsel, const int32_t* sel,
   const int boned = (y1 && p->r1max > 0) ? ceil_div(p->r1max, 64) : 0;
   if (bpull + boned == 0) return MDP_OK;
   dim3 grid(bpull + boned, nsel);
-  ::mdp::launch_k(coupling_phase2_kernel, grid, 256, 0, st, *p, sel, bpull, s, alpha, y3, ld, div, x1, y1);
+  static const int dep = env_int("MDP_PHASE2_PDL", 1);
+  if (dep)
+    ::mdp::launch_k_dependent(coupling_phase2_kernel, grid, 256, 0, st, *p, sel, bpull, s, alpha, y3, ld, div, x1, y1);
+  else
+    ::mdp::launch_k(coupling_phase2_kernel, grid, 256, 0, st, *p, sel, bpull, s, alpha, y3, ld, div, x1, y1);
   MDP_LAUNCH_CHECK("coupling_phase2_kernel");
   return MDP_OK;
 }
