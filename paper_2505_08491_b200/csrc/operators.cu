@@ -433,7 +433,9 @@ __global__ void __launch_bounds__(256, (N > 160 && N <= 224 && !JAC) ? 2 : STENC
                                                         const double* __restrict__ jr, double omega,
                                                         const GatherArgs G) {
   using namespace async;
-  MDP_PDL_ENTER();
+  // launched as a programmatic dependent: everything up to the ring set-up (barrier init, zeroing the
+  // stages) touches shared memory only and runs before the wait on the previous grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   constexpr int NR = RY + 2;
   const int n = N > 0 ? N : P.n;
   // grid (x: block slot, y: system): slots [0, gx) run the Pi gather (first in
@@ -442,6 +444,7 @@ __global__ void __launch_bounds__(256, (N > 160 && N <= 224 && !JAC) ? 2 : STENC
   const int s = sys_of(sel, blockIdx.y);
   const int gx = G.s_out ? G.nblk : 0;
   if ((int)blockIdx.x < gx) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     gather_rows(P, s, blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), gx * (blockDim.x >> 5), G.x3, G.x1, ldx,
                 G.s_out);
     return;
@@ -461,7 +464,7 @@ __global__ void __launch_bounds__(256, (N > 160 && N <= 224 && !JAC) ? 2 : STENC
   const int j = (slot % bands) * RY;
   const int z0 = (slot / bands) * zchunk;
   const int z1 = min(n, z0 + zchunk);
-  if (j >= n || z0 >= n) return;  // gather-slice width / chunk rounding
+  if (j >= n || z0 >= n) return;  // gather-slice width / chunk rounding (touches no memory)
   const bool dir = P.bc3d != 0;
   int trc = -1;
 #ifdef ST3_TRACE
@@ -483,6 +486,7 @@ __global__ void __launch_bounds__(256, (N > 160 && N <= 224 && !JAC) ? 2 : STENC
   // by 0) must see finite values
   for (int t = threadIdx.x; t < kSt3 * sws + 2; t += blockDim.x) stg[t - 2] = 0.0;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes before the async-proxy copies
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // x (and r, for the Jacobi sweep) come from the previous grid
   __syncthreads();
   ST3_TR(trc, 1);
   const double* xp = x + (int64_t)s * ldx;
@@ -745,12 +749,22 @@ static void launch_stencil3_t(dim3 grid, int threads, size_t smem, cudaStream_t 
                               const int32_t* sel, const double* x, int64_t ldx, double* y, int64_t ldy, int zchunk,
                               const double* jr, double omega, const GatherArgs& G) {
   launch_stencil3_attr<N, RY>();
-  if (jr)
-    ::mdp::launch_k(stencil3_kernel<N, RY, true>, grid, threads, smem, st, *p, sel, x, ldx, y, ldy, zchunk, jr, omega,
-                    G);
-  else
-    ::mdp::launch_k(stencil3_kernel<N, RY, false>, grid, threads, smem, st, *p, sel, x, ldx, y, ldy, zchunk, jr,
-                    omega, G);
+  static const int dep = env_int("MDP_STENCIL_PDL", 1);
+  if (jr) {
+    if (dep)
+      ::mdp::launch_k_dependent(stencil3_kernel<N, RY, true>, grid, threads, smem, st, *p, sel, x, ldx, y, ldy, zchunk,
+                                jr, omega, G);
+    else
+      ::mdp::launch_k(stencil3_kernel<N, RY, true>, grid, threads, smem, st, *p, sel, x, ldx, y, ldy, zchunk, jr, omega,
+                      G);
+  } else {
+    if (dep)
+      ::mdp::launch_k_dependent(stencil3_kernel<N, RY, false>, grid, threads, smem, st, *p, sel, x, ldx, y, ldy, zchunk,
+                                jr, omega, G);
+    else
+      ::mdp::launch_k(stencil3_kernel<N, RY, false>, grid, threads, smem, st, *p, sel, x, ldx, y, ldy, zchunk, jr,
+                      omega, G);
+  }
 }
 
 // resident blocks per SM of one instantiation at this launch shape (registers AND shared memory;
