@@ -172,6 +172,11 @@ def pack_conv(kernel: np.ndarray, path: int) -> np.ndarray:
     nch = cin // (4 * cqc)
     if cout <= 64:  # z-tap fold (unet_tc.cu issue_stage_fold): [chunk][dydx][quad][dz][cout][4]
         p = k.reshape(cout, nch, cqc, 4, 3, 9).transpose(1, 5, 2, 4, 0, 3)
+        # followed by the same pack of the filter with dy and dz exchanged: the row-remainder launch
+        # of odd grids runs the kernel on a (x, z, y) view of the activations (unet_tc.cu tc_conv3)
+        kp = np.asarray(kernel, dtype=np.float32).transpose(0, 1, 3, 2, 4).reshape(cout, cin, 27)
+        pp = kp.reshape(cout, nch, cqc, 4, 3, 9).transpose(1, 5, 2, 4, 0, 3)
+        return tf32_round(np.concatenate([np.ascontiguousarray(p).ravel(), np.ascontiguousarray(pp).ravel()]))
     else:
         p = k.reshape(cout, nch, cqc, 4, 27).transpose(1, 4, 2, 0, 3)  # [chunk][tap][quad][cout][4]
     return tf32_round(np.ascontiguousarray(p))

@@ -98,11 +98,14 @@ def test_weight_packing_layouts():
     k128 = rng.standard_normal((128, 32, 3, 3, 3)).astype(np.float32)  # Cout = 128: [chunk][tap][quad][cout][4]
     p0 = neural.pack_conv(k128, neural.PATH_TCGEN05).reshape(2, 27, 4, 128, 4)
     assert abs(p0[1, 13, 2, 40, 3] - k128[40, 16 + 2 * 4 + 3].ravel()[13]) <= 2e-3 * abs(k128[40, 27].ravel()[13])
-    p64 = neural.pack_conv(k, neural.PATH_TCGEN05).reshape(2, 9, 4, 3, 64, 4)  # Cout <= 64: z-tap fold layout
-    assert abs(p64[1, 4, 2, 1, 40, 3] - k[40, 16 + 2 * 4 + 3, 1, 1, 1]) <= 2e-3 * abs(k[40, 27, 1, 1, 1])
+    # Cout <= 64: z-tap fold layout, followed by the same pack of the dy <-> dz exchanged filter
+    p64 = neural.pack_conv(k, neural.PATH_TCGEN05).reshape(2, 2, 9, 4, 3, 64, 4)
+    assert abs(p64[0, 1, 4, 2, 1, 40, 3] - k[40, 16 + 2 * 4 + 3, 1, 1, 1]) <= 2e-3 * abs(k[40, 27, 1, 1, 1])
     k32 = rng.standard_normal((32, 64, 3, 3, 3)).astype(np.float32)  # Cout = 32: z-tap fold layout
-    pf = neural.pack_conv(k32, neural.PATH_TCGEN05).reshape(4, 9, 4, 3, 32, 4)  # [chunk][dydx][quad][dz][cout][4]
-    assert abs(pf[2, 7, 1, 2, 30, 3] - k32[30, 2 * 16 + 1 * 4 + 3, 2, 2, 1]) <= 1e-3 * abs(k32[30, 39, 2, 2, 1])
+    pf = neural.pack_conv(k32, neural.PATH_TCGEN05).reshape(2, 4, 9, 4, 3, 32, 4)  # [copy][chunk][dydx][quad][dz][cout][4]
+    assert abs(pf[0, 2, 7, 1, 2, 30, 3] - k32[30, 2 * 16 + 1 * 4 + 3, 2, 2, 1]) <= 1e-3 * abs(k32[30, 39, 2, 2, 1])
+    # permuted copy: unit 7 = (line offset 2, dx 1), plane offset 0 -> physical (dz, dy, dx) = (2, 0, 1)
+    assert abs(pf[1, 2, 7, 1, 0, 30, 3] - k32[30, 39, 2, 0, 1]) <= 1e-3 * abs(k32[30, 39, 2, 0, 1])
     t = rng.standard_normal((64, 32, 2, 2, 2)).astype(np.float32)
     pt = neural.pack_tconv(t).reshape(2, 64, 8, 16)
     assert pt[1, 10, 5, 3] == t[10, 16 + 3].ravel()[5]

@@ -129,6 +129,28 @@ def test_unet_forward_large_vs_oracle(gpu, n):
     assert rel(y, ref) <= TF32_TOL
 
 
+def test_unet_forward_row_remainder_vs_fp32_path(gpu):
+    """n = 113 = 16 * 7 + 1: the Cout <= 64 layers compute their last y-row in a second launch on a (x, z, y)
+    view with the dy <-> dz permuted filter copy (unet_tc.cu tc_conv3); checked against the FP32 CUDA-core path
+    (itself pinned to the oracle at the smaller sizes), and 129 goes through the same code vs the reference
+    (tests/test_gpu_large.py)."""
+    from paper_2505_08491_b200 import neural
+    n = 113
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((1, 2, n, n, n))
+    x[0, 0] /= np.linalg.norm(x[0, 0])
+    x[0, 1] = np.abs(x[0, 1]) * 0.2
+    p = neural.perturbed_params(1)
+    y0 = neural.unet_forward(p, x, path=0)
+    y1 = neural.unet_forward(p, x, path=1)
+    assert rel(y0, y1) <= TF32_TOL
+    a, b = y0.reshape(n, n, n), y1.reshape(n, n, n)  # (z, y, x)
+    # the last row / plane / column in particular
+    assert rel(a[:, n - 1, :], b[:, n - 1, :]) <= TF32_TOL
+    assert rel(a[n - 1], b[n - 1]) <= TF32_TOL
+    assert rel(a[:, :, n - 1], b[:, :, n - 1]) <= TF32_TOL
+
+
 def test_shipped_init_is_zero_map(gpu):
     from paper_2505_08491_b200 import neural
     x = np.random.default_rng(0).standard_normal((2, 9, 9, 9))
