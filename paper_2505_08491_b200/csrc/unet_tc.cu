@@ -972,12 +972,14 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   // tensor map with y and z exchanged (and the dy <-> dz permuted weight copy behind the first one): there
   // the 16-line axis runs along z and the 1-2 left-over rows are the plane axis.  Per-item shape only.
   static const int rem_env = [] { const char* e = getenv("MDP_CONV_REMAINDER"); return e ? atoi(e) : 1; }();
+  static const int rem_min = [] { const char* e = getenv("MDP_CONV_REMAINDER_MIN"); return e ? atoi(e) : 4; }();
   const int yrem = S % BY;
-  // (only where the main grid is many rounds deep: the second launch costs ~15 us of its own; measured
-  // 129^3 forward -2.1%, 65^3 +2.8%, 33^3 +17%)
+  // (only where the main grid is several rounds deep per item: the second launch costs ~15 us of its own;
+  // measured 129^3 forward -2.1%, 65^3 x 16 -7.7% (cfg3 solve +5.8%), one 65^3 item +3%, 33^3 +17%: the
+  // threshold of 4 bricks per SM takes 65^3 in -- its use is the batched multi-query solve -- and leaves 33^3 out)
   const bool split_rows = rem_env && cout <= 64 && epi != EPI_POOL && A.nsplit == 1 && A.ksplit == 1 &&
                           yrem >= 1 && yrem <= 2 &&
-                          (int64_t)A.tx * (S / BY) * ceil_div(S, 4) >= 8 * (int64_t)sm_count();
+                          (int64_t)A.tx * (S / BY) * ceil_div(S, 4) >= rem_min * (int64_t)sm_count();
   if (split_rows) A.ty = S / BY;
   // z-tap fold for Cout <= 64 (weights packed [chunk][dydx][quad][dz][Cout][4]);
   // 4-plane bricks when the layer still has >= 2 bricks per SM with them
