@@ -697,7 +697,7 @@ struct TconvArgs {
   uint32_t a_bytes, b_bytes, tmem_cols;
 };
 
-__global__ void __launch_bounds__(192, 1) tconv_tc_kernel(const TconvArgs T) {
+__global__ void __launch_bounds__(320, 1) tconv_tc_kernel(const TconvArgs T) {
   MDP_PDL_ENTER();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int grp = blockIdx.y;
@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(192, 1) tconv_tc_kernel(const TconvArgs T) {
       mbar_init(&afull[i], 1);
       mbar_init(&aempty[i], 1);
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], blockDim.x - 64);  // every epilogue thread (4 or 8 warps) arrives
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -785,6 +785,10 @@ __global__ void __launch_bounds__(192, 1) tconv_tc_kernel(const TconvArgs T) {
     }
   } else {  // ---- epilogue warps 2..5: TMEM lanes 32 (warp % 4) ..
     const int quarter = warp & 3;
+    // 8 epilogue warps (wide inputs): warps 2-5 / 6-9, the two warps of a TMEM lane quarter split the tile's
+    // items by parity (65^3: both transposed convs 36 -> 28 us); small inputs launch 4 (33^3: 16 vs 18 us with 8)
+    const bool two = blockDim.x > 192;
+    const int eh = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
     const int So = 2 * Sin + T.op;
@@ -807,6 +811,7 @@ __global__ void __launch_bounds__(192, 1) tconv_tc_kernel(const TconvArgs T) {
           const int tap = grp * T.tg + t;
           const int64_t o = ((int64_t)(2 * z + (tap >> 2)) * So + 2 * y + ((tap >> 1) & 1)) * So + 2 * x;
           for (int cg = 0; cg < T.cout / 16; ++cg) {
+            if (two && (((t >> 1) * (T.cout / 16) + cg) & 1) != eh) continue;
             float r0[16], r1[16];
             tmem_ld16(d0 + (uint32_t)(t * T.cout + cg * 16), r0);
             tmem_ld16(d0 + (uint32_t)((t + 1) * T.cout + cg * 16), r1);
@@ -833,6 +838,7 @@ __global__ void __launch_bounds__(192, 1) tconv_tc_kernel(const TconvArgs T) {
         const int tap = grp * T.tg + t;
         const int64_t o = ((int64_t)(2 * z + (tap >> 2)) * So + 2 * y + ((tap >> 1) & 1)) * So + 2 * x + (tap & 1);
         for (int cg = 0; cg < T.cout / 16; ++cg) {
+          if (two && ((t * (T.cout / 16) + cg) & 1) != eh) continue;
           float r[16];
           tmem_ld16(d0 + (uint32_t)(t * T.cout + cg * 16), r);
 #pragma unroll
@@ -1225,7 +1231,7 @@ int tc_tconv(int nb, const float4* in, int in_cq, int cin, int cout, int Sin, in
     attr_set = true;
   }
   dim3 grid(ncta + npad, groups, 1);
-  ::mdp::launch_k(tconv_tc_kernel, grid, 192, smem, st, T);
+  ::mdp::launch_k(tconv_tc_kernel, grid, Sin >= 32 ? 320 : 192, smem, st, T);
   MDP_LAUNCH_CHECK("tconv_tc_kernel");
   return MDP_OK;
 }
