@@ -79,6 +79,8 @@ struct ConvArgs {
   int tps;       // taps (fold: (dy,dx) units) per weight stage (one mbarrier handshake per stage)
   int fold;      // Cout == 32: the 3 z-taps of one (dy,dx) are one N = 3*32 weight block (see issue_stage_fold)
   uint32_t tmem_cols;
+  int tail_wait;      // row-remainder launch: a programmatic dependent of the main launch that does NOT wait for it
+                      // before working (same input, disjoint output rows) but before it exits (see tc_conv3)
   int perm, zoff;     // perm: the tensor map's dims are (x, z, y): the kernel's 16-line axis is the physical z and
                       // its plane axis the physical y, planes starting at zoff (remainder rows of odd grids)
   int pair;           // enc1a (Cin = 2): x-shifted input quads, one K = 8 MMA per (dy, halo plane) (see issue_stage_pair)
@@ -326,7 +328,7 @@ __global__ void __launch_bounds__(384, 1) conv3_tc_kernel(const __grid_constant_
   // weights are never written on the device, so their producer (warp 0) streams the first
   // stages without waiting for it either
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (warp != 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (warp != 0 && !A.tail_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
   const int nunits = A.pair ? 3 : (A.fold ? 9 : 27);
 
   if (warp == 3) {
@@ -582,6 +584,9 @@ __global__ void __launch_bounds__(384, 1) conv3_tc_kernel(const __grid_constant_
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(A.tmem_cols));
   }
+  // the remainder launch ran beside the main launch's tail; it may only COMPLETE after it, so that the next
+  // kernel in the stream (which waits for this grid) sees both
+  if (A.tail_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
 #ifdef CONV_TRACE
   if (threadIdx.x == 0 && blockIdx.x == 0 && A.cin == g_trace_sel[0] && A.cout == g_trace_sel[1]) g_trace[1] = clock64();
 #endif
@@ -1096,7 +1101,15 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
     MDP_REQUIRE(rp == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d) for the row remainder of S=%d", (int)rp, S);
     const size_t smem2 = 1024 + (size_t)B.na * B.a_bytes + (size_t)nbs * B.b_bytes + 2048;
     const int grid2 = B.ntiles < sm_count() ? B.ntiles : sm_count();
-    ::mdp::launch_k(conv3_tc_kernel<2>, grid2, 384, smem2, st, pmap, wmap, B);
+    static const int overlap = [] { const char* e = getenv("MDP_CONV_REMAINDER_OVERLAP"); return e ? atoi(e) : 1; }();
+    if (overlap) {
+      // its CTAs take the SMs the main launch's last round leaves idle (4488 bricks on 148 SMs: a
+      // one-brick tail on 70% of them)
+      B.tail_wait = 1;
+      ::mdp::launch_k_dependent(conv3_tc_kernel<2>, grid2, 384, smem2, st, pmap, wmap, B);
+    } else {
+      ::mdp::launch_k(conv3_tc_kernel<2>, grid2, 384, smem2, st, pmap, wmap, B);
+    }
     MDP_LAUNCH_CHECK("conv3_tc_kernel (row remainder)");
   }
   if (A.ksplit > 1 && epi == EPI_HEAD) {
