@@ -271,7 +271,14 @@ int mdp_dense_matvec(int32_t n, const double* M, const double* x, double* y, voi
 typedef struct mdp_unet {
   int32_t n;        /* spatial size (points per edge)                      */
   int32_t path;     /* 0: tcgen05 TF32 implicit GEMM, 1: CUDA-core FP32 check path */
-  const float* w[11];  /* packed weights, ARCHITECTURE order */
+  const float* w[11];  /* packed weights, ARCHITECTURE order (path 0:
+                          TF32-rounded, 3x3x3 layers with Cout <= 64 as
+                          [chunk][dydx][quad][dz][Cout][4] FOLLOWED by the same pack of
+                          the filter with dy and dz exchanged (the row-remainder launch
+                          of odd grids reads it at offset Cin*Cout*27 floats), Cout = 128
+                          as [chunk][tap][quad][Cout][4], enc1a raw [16][2][27],
+                          transposed convs [tap][quad][Cout][4]; as written by
+                          paper_2505_08491_b200.neural.pack_conv / pack_tconv) */
   const float* b[11];  /* biases (NULL where the layer has none)           */
   int32_t accumulate;  /* 1: z_s += scale_i * U(..) (fused z + z_net of the
                           smoothed apply, training.py:305-311); 0: z_s = ...  */
@@ -289,7 +296,7 @@ int mdp_unet_apply(const mdp_unet* net, int32_t nb, const int32_t* sel, const do
                    int64_t ldz, void* workspace, size_t ws_bytes, void* stream);
 
 /* Single-layer entry points used by the parity tests (float32 C4-blocked
- * activations [b][C/4][S][S][S][4]). */
+ * activations [b][C/4][S][S][S][4]; w packed as in mdp_unet.w). */
 int mdp_conv3_layer(int32_t path, int32_t nb, int32_t S, int32_t cin, int32_t cout,
                     const float* in, int32_t in_cq, int32_t in_q0, const float* w, const float* bias,
                     int32_t relu, float* out, int32_t out_cq, int32_t out_q0, int32_t pool,
