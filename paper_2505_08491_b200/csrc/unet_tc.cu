@@ -999,6 +999,11 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
   // FP32 accumulation order, so batched == serial stays bitwise (training.py:322-338)
   const int zp = (A.fold && A.ksplit == 1 && (int64_t)A.tx * A.ty * ceil_div(Sc, 4) >= 2 * sm_count()) ? 4 : 2;
   A.tz = ceil_div(Sc, zp);
+  // likewise the plane remainder of 4-plane bricks (S = 4 k + 1: the last brick of every column would
+  // carry one useful plane of four): planes [4 floor(S/4), S) go to a third, 2-plane launch
+  const int zrem = S % 4;
+  const bool split_planes = split_rows && zp == 4 && zrem >= 1 && zrem <= 2;
+  if (split_planes) A.tz = S / 4;
   const int spatial = nb * A.tx * A.ty * A.tz;
   A.cps = A.nchunk / A.ksplit;
   A.ntiles = spatial * A.nsplit * A.ksplit;
@@ -1111,6 +1116,25 @@ int tc_conv3(int nb, int S, int cin, int cout, const float4* in, int in_cq, int 
       ::mdp::launch_k(conv3_tc_kernel<2>, grid2, 384, smem2, st, pmap, wmap, B);
     }
     MDP_LAUNCH_CHECK("conv3_tc_kernel (row remainder)");
+    if (split_planes) {
+      ConvArgs C = A;  // normal orientation, rows below the row remainder, the last 1-2 planes
+      C.zoff = (S / 4) * 4;
+      C.tz = 1;
+      C.ntiles = nb * C.tx * C.ty * C.tz;
+      C.a_bytes = (uint32_t)C.cqc * Brick<2>::QUAD_BYTES;
+      C.tail_wait = overlap ? 1 : 0;
+      CUtensorMap zmap;
+      CUresult rz = enc(&zmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)in, gdim, gstride, pbox, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      MDP_REQUIRE(rz == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d) for the plane remainder of S=%d", (int)rz, S);
+      const int grid3 = C.ntiles < sm_count() ? C.ntiles : sm_count();
+      if (overlap)
+        ::mdp::launch_k_dependent(conv3_tc_kernel<2>, grid3, 384, smem2, st, zmap, wmap, C);
+      else
+        ::mdp::launch_k(conv3_tc_kernel<2>, grid3, 384, smem2, st, zmap, wmap, C);
+      MDP_LAUNCH_CHECK("conv3_tc_kernel (plane remainder)");
+    }
   }
   if (A.ksplit > 1 && epi == EPI_HEAD) {
     const int64_t total = (int64_t)nb * S * S * S;
