@@ -454,12 +454,26 @@ __global__ void arnoldi_next_kernel(const int32_t* sel, double* V, int64_t ldv_s
   double* dst = nv <= kmax ? V + s * ldv_sys + nv * ldv_vec : nullptr;
   const double* ws = w + s * ldw;
   double* vc = vcur ? vcur + s * ldc : nullptr;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    double v = ws[e] / hn;
-    if (dst) dst[e] = v;
-    if (vc) vc[e] = v;
-    if (J.out) J.out[s * ldc + e] = (J.omega * v) / J.diag[s * ldc + e];
+  // four independent loads per thread in flight (one 8-byte load per grid-stride step left the
+  // 17 MB vectors at ~2 TB/s: too few bytes in flight for the HBM latency)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 < n; e0 += 4 * stride) {
+    double wv[4], dg[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t e = e0 + k * stride;
+      wv[k] = e < n ? ws[e] : 0.0;
+      dg[k] = (J.out && e < n) ? J.diag[s * ldc + e] : 1.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t e = e0 + k * stride;
+      if (e >= n) break;
+      const double v = wv[k] / hn;
+      if (dst) dst[e] = v;
+      if (vc) vc[e] = v;
+      if (J.out) J.out[s * ldc + e] = (J.omega * v) / dg[k];
+    }
   }
 }
 
@@ -538,10 +552,22 @@ __global__ void __launch_bounds__(128) residual_kernel(const int32_t* sel, const
   const int s = sys_of(sel, i);
   const int64_t e0 = blockIdx.x * chunk, e1 = min(n, e0 + chunk);
   double acc = 0.0;
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    double v = b[s * ld + e] - y[s * ld + e];
-    r[s * ld + e] = v;
-    acc += v * v;
+  for (int64_t ea = e0 + threadIdx.x; ea < e1; ea += 4 * (int64_t)blockDim.x) {  // 8 loads in flight, same sum order
+    double bv[4], yv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t e = ea + k * (int64_t)blockDim.x;
+      bv[k] = e < e1 ? b[s * ld + e] : 0.0;
+      yv[k] = e < e1 ? y[s * ld + e] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t e = ea + k * (int64_t)blockDim.x;
+      if (e >= e1) break;
+      const double v = bv[k] - yv[k];
+      r[s * ld + e] = v;
+      acc += v * v;
+    }
   }
   double t = block_sum(acc, sh);
   if (threadIdx.x == 0) mine[0] = t;
@@ -567,9 +593,15 @@ __global__ void copy_vec_kernel(const int32_t* sel, const double* __restrict__ s
   const int s = sys_of(sel, i);
   const double* a = src + s * lds;
   double* d = dst + s * ldd + (slot ? (int64_t)slot[i] * slot_stride : 0);
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x)
-    d[e] = a[e];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 < n; e0 += 4 * stride) {
+    double v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = e0 + k * stride < n ? a[e0 + k * stride] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (e0 + k * stride < n) d[e0 + k * stride] = v[k];
+  }
 }
 
 // ILU(0) sweeps, one CTA per system, level-scheduled.  The per-row
@@ -815,11 +847,25 @@ __global__ void fixed_start_kernel(const int32_t* sel, const double* __restrict_
   const double* bs = b + s * ldb;
   double* vs = v0 + s * ldv;
   double* cs = vcur + s * ldc;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const double v = bs[e] / beta[i];
-    vs[e] = v;
-    cs[e] = v;
-    if (J.out) J.out[s * ldc + e] = (J.omega * v) / J.diag[s * ldc + e];
+  const double bi = beta[i];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 < n; e0 += 4 * stride) {
+    double bv[4], dg[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t e = e0 + k * stride;
+      bv[k] = e < n ? bs[e] : 0.0;
+      dg[k] = (J.out && e < n) ? J.diag[s * ldc + e] : 1.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t e = e0 + k * stride;
+      if (e >= n) break;
+      const double v = bv[k] / bi;
+      vs[e] = v;
+      cs[e] = v;
+      if (J.out) J.out[s * ldc + e] = (J.omega * v) / dg[k];
+    }
   }
 }
 
@@ -838,10 +884,18 @@ __global__ void fixed_finish_kernel(const int32_t* sel, int m, const double* __r
   __syncthreads();
   const double* Zs = Z + s * ldz_sys;
   double* xs = x + s * ldx;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    double t = 0.0;
-    for (int k = 0; k < m; ++k) t += __ldg(Zs + k * ldz_vec + e) * ysh[k];
-    xs[e] = 0.0 + t;  // as fill(0) followed by basis_update's x += t
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 < n; e0 += 2 * stride) {
+    const int64_t e1 = e0 + stride;  // two elements per thread: 2 m loads in flight
+    double t0 = 0.0, t1 = 0.0;
+    for (int k = 0; k < m; ++k) {
+      const double z0 = __ldg(Zs + k * ldz_vec + e0);
+      const double z1 = e1 < n ? __ldg(Zs + k * ldz_vec + e1) : 0.0;
+      t0 += z0 * ysh[k];
+      t1 += z1 * ysh[k];
+    }
+    xs[e0] = 0.0 + t0;  // as fill(0) followed by basis_update's x += t
+    if (e1 < n) xs[e1] = 0.0 + t1;
   }
 }
 
@@ -866,7 +920,7 @@ __global__ void fill_kernel(const int32_t* sel, double* y, int64_t ld, int64_t n
 
 inline dim3 ew_grid(int64_t n, int nsel) {
   int bx = ceil_div(n, 256);
-  int cap = 4 * sm_count();
+  int cap = 8 * sm_count();  // 2048 resident threads per SM; the hot loops also keep 4 loads per thread in flight
   bx = bx > cap ? cap : bx;
   return dim3(bx < 1 ? 1 : bx, nsel);
 }
