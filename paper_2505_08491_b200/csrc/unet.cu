@@ -30,12 +30,27 @@ __global__ void pack_input_kernel(const int32_t* sel, const double* __restrict__
   if (shifted) {
     // tensor-core enc1a (tc_enc1a): quad of voxel x = (r, d)[x] | (r, d)[x+1] (zero past the row end), TF32-rounded
     float4* x4 = reinterpret_cast<float4*>(xin);
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
-         v += (int64_t)gridDim.x * blockDim.x) {
-      const bool nxt = (int)(v % S) + 1 < S;
-      const double r0 = r[s * ld + v] / den, r1 = nxt ? r[s * ld + v + 1] / den : 0.0;
-      const double d0 = dist[s * ldd + v], d1 = nxt ? dist[s * ldd + v + 1] : 0.0;
-      x4[b * nvox + v] = tf32_round4(make_float4((float)r0, (float)d0, (float)r1, (float)d1));
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v0 < nvox; v0 += 4 * stride) {
+      double ra[4], rb[4], da[4], db[4];  // sixteen loads in flight per thread before the divisions
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t v = v0 + k * stride;
+        const bool in = v < nvox;
+        const bool nxt = in && (int)(v % S) + 1 < S;
+        ra[k] = in ? r[s * ld + v] : 0.0;
+        rb[k] = nxt ? r[s * ld + v + 1] : 0.0;
+        da[k] = in ? dist[s * ldd + v] : 0.0;
+        db[k] = nxt ? dist[s * ldd + v + 1] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t v = v0 + k * stride;
+        if (v >= nvox) break;
+        const bool nxt = (int)(v % S) + 1 < S;
+        const double r0 = ra[k] / den, r1 = nxt ? rb[k] / den : 0.0;
+        x4[b * nvox + v] = tf32_round4(make_float4((float)r0, (float)da[k], (float)r1, (float)db[k]));
+      }
     }
     return;
   }
