@@ -300,9 +300,14 @@ __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* 
                                                   const double* __restrict__ jrp, const double* __restrict__ dgp,
                                                   double omega, int n, int i, int j, int z0, int z1,
                                                   const StencilCoef& K, const double* stg, int sw, int swj,
-                                                  uint64_t* full, uint64_t* empty, int r_lo, int r_hi, int trc) {
+                                                  uint64_t* full, uint64_t* empty, int r_lo, int r_hi, int trc,
+                                                  const double* __restrict__ xgp, bool lastcol) {
   using namespace async;
   constexpr int NR = RY + 2;
+  // Dirichlet cube with n = 32 t + 1 columns (plain stencil): the band runs t consumer warps and the lane of
+  // column n - 2 also writes column n - 1, an eliminated identity node (y = x), instead of a further warp
+  // with one live column
+  const bool lc_lane = DIR && lastcol && i == n - 2;
   const int lane = threadIdx.x & 31;
   const int nn = n * n;
   const bool col_in = i < n;
@@ -362,6 +367,15 @@ __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* 
         for (int r = 0; r < RY; ++r) {
           jv[r] = jb[r * n];
           dv[r] = jb[swj + r * n];
+        }
+      }
+      if (!JAC && DIR && lc_lane && k >= z0 && k < z1) {
+        // column n - 1 of plane k needs no recurrence: y = x there, and the raw value sits in this stage
+        // (the right neighbour of this lane's column)
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          if (EDGE && j + r >= n) continue;
+          yp[(int64_t)k * nn + (int64_t)(j + r) * n + (n - 1)] = b[roff[r + 1] + 1];
         }
       }
       __syncwarp();
@@ -427,7 +441,7 @@ __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* 
 // variant spills ~400 B at 128 and loses, so it keeps its registers).  The 6-warp blocks of 129^3 already hold
 // two; squeezing a third in (112 registers) costs more in spills than the occupancy returns.
 template <int N, int RY, bool JAC>
-__global__ void __launch_bounds__(256, (N > 160 && N <= 224 && !JAC) ? 2 : STENCIL3_MINB) stencil3_kernel(const mdp_problem P, const int32_t* sel,
+__global__ void __maxnreg__((N == 129 && !JAC) ? 136 : ((N > 160 && N <= 224 && !JAC) ? 128 : 255)) stencil3_kernel(const mdp_problem P, const int32_t* sel,
                                                         const double* __restrict__ x, int64_t ldx,
                                                         double* __restrict__ y, int64_t ldy, int zchunk,
                                                         const double* __restrict__ jr, double omega,
@@ -457,7 +471,10 @@ __global__ void __launch_bounds__(256, (N > 160 && N <= 224 && !JAC) ? 2 : STENC
   const int sw = (NR * n + 4 + 1) & ~1;  // x-band stride in doubles (16-byte multiple)
   const int swj = JAC ? ((RY * n + 3) & ~1) : 0;  // r / diag(C) bands of the emitted plane (Jacobi epilogue)
   const int sws = sw + 2 * swj;              // whole stage
-  const int tiles_x = (n + 31) / 32;
+  // (plain stencil only: the Jacobi sweep would need r at that node ahead of its stage -- a global load
+  // per step on the critical path cost it 35% -- and keeps the extra warp)
+  const bool lastcol = !JAC && P.bc3d != 0 && n > 32 && ((n - 1) & 31) == 0;
+  const int tiles_x = lastcol ? (n - 1) / 32 : (n + 31) / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bands = (n + RY - 1) / RY;
   const int slot = blockIdx.x - gx;
@@ -535,7 +552,8 @@ __global__ void __launch_bounds__(256, (N > 160 && N <= 224 && !JAC) ? 2 : STENC
   const int lo = dir ? 1 : 0, hi = dir ? n - 2 : n - 1;
   const bool edge = (j - 1 < lo) || (j + RY > hi);
 #define MDP_ST3(D, E) \
-  stencil3_consumer<N, RY, JAC, D, E>(P, yp, jrp, dgp, omega, n, i, j, z0, z1, K, stg, sw, swj, full, empty, r_lo, r_hi, trc)
+  stencil3_consumer<N, RY, JAC, D, E>(P, yp, jrp, dgp, omega, n, i, j, z0, z1, K, stg, sw, swj, full, empty, r_lo, r_hi, trc, \
+                                      xp, lastcol)
   if (dir) {
     if (edge) MDP_ST3(true, true); else MDP_ST3(true, false);
   } else {
@@ -773,7 +791,8 @@ template <int N, int RY>
 static int stencil3_blocks_per_sm(int threads, size_t smem, bool jac, int n) {
   static int cache[2][2] = {{0, 0}, {0, 0}};  // [jac] -> (n, blocks)
   int* c = cache[jac ? 1 : 0];
-  if (c[0] == n && c[1] > 0) return c[1];
+  const int key = n * 2048 + threads;
+  if (c[0] == key && c[1] > 0) return c[1];
   launch_stencil3_attr<N, RY>();
   int nb = 0;
   cudaError_t e = jac ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, stencil3_kernel<N, RY, true>, threads, smem)
@@ -782,7 +801,7 @@ static int stencil3_blocks_per_sm(int threads, size_t smem, bool jac, int n) {
     cudaGetLastError();
     nb = 1;
   }
-  c[0] = n;
+  c[0] = key;
   c[1] = nb;
   return nb;
 }
@@ -796,7 +815,8 @@ static int launch_stencil3(const mdp_problem* p, int32_t nsel, const int32_t* se
   static const int ry_env = env_int("MDP_STENCIL_RY", 0);
   const int RY = ry_env == 2 || ry_env == 4 || ry_env == 8 ? ry_env : (n <= 48 ? 2 : 4);
   const int S = kSt3;
-  const int tiles_x = ceil_div(n, 32);
+  const bool lastcol = jr == nullptr && p->bc3d != 0 && n > 32 && ((n - 1) & 31) == 0;  // see stencil3_consumer
+  const int tiles_x = lastcol ? (n - 1) / 32 : ceil_div(n, 32);
   const int bands = ceil_div(n, RY);
   const int threads = 32 * (tiles_x + 1);
   const size_t sw = (size_t)(((RY + 2) * n + 4 + 1) & ~1);
