@@ -440,8 +440,8 @@ __device__ __forceinline__ void stencil3_consumer(const mdp_problem& P, double* 
 // spills) two do: K00 stencil 193^3 x 8 0.72 -> 0.86 of HBM, coupled SpMV 0.63 -> 0.74 (the Jacobi
 // variant spills ~400 B at 128 and loses, so it keeps its registers).  The 6-warp blocks of 129^3 already hold
 // two; squeezing a third in (112 registers) costs more in spills than the occupancy returns.
-template <int N, int RY, bool JAC>
-__global__ void __maxnreg__((N == 129 && !JAC) ? 136 : ((N > 160 && N <= 224 && !JAC) ? 128 : 255)) stencil3_kernel(const mdp_problem P, const int32_t* sel,
+template <int N, int RY, bool JAC, bool LC = false>
+__global__ void __maxnreg__((N == 129 && LC) ? 136 : ((N > 160 && N <= 224 && !JAC) ? 128 : 255)) stencil3_kernel(const mdp_problem P, const int32_t* sel,
                                                         const double* __restrict__ x, int64_t ldx,
                                                         double* __restrict__ y, int64_t ldy, int zchunk,
                                                         const double* __restrict__ jr, double omega,
@@ -473,7 +473,10 @@ __global__ void __maxnreg__((N == 129 && !JAC) ? 136 : ((N > 160 && N <= 224 && 
   const int sws = sw + 2 * swj;              // whole stage
   // (plain stencil only: the Jacobi sweep would need r at that node ahead of its stage -- a global load
   // per step on the critical path cost it 35% -- and keeps the extra warp)
-  const bool lastcol = !JAC && P.bc3d != 0 && n > 32 && ((n - 1) & 31) == 0;
+  // LC: chosen by the launcher for batches of plain stencils (a single system's coupled SpMV, with the gather
+  // folded into this launch, measured 2 us slower with it; at 129^3 the instantiation is capped at 136
+  // registers so that three 5-warp blocks fit an SM)
+  constexpr bool lastcol = LC && !JAC;
   const int tiles_x = lastcol ? (n - 1) / 32 : (n + 31) / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bands = (n + RY - 1) / RY;
@@ -758,6 +761,7 @@ static void launch_stencil3_attr() {
   if (!attr) {
     cudaFuncSetAttribute(stencil3_kernel<N, RY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(stencil3_kernel<N, RY, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(stencil3_kernel<N, RY, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
 }
@@ -765,10 +769,17 @@ static void launch_stencil3_attr() {
 template <int N, int RY>
 static void launch_stencil3_t(dim3 grid, int threads, size_t smem, cudaStream_t st, const mdp_problem* p,
                               const int32_t* sel, const double* x, int64_t ldx, double* y, int64_t ldy, int zchunk,
-                              const double* jr, double omega, const GatherArgs& G) {
+                              const double* jr, double omega, const GatherArgs& G, bool lastcol) {
   launch_stencil3_attr<N, RY>();
   static const int dep = env_int("MDP_STENCIL_PDL", 1);
-  if (jr) {
+  if (!jr && lastcol) {
+    if (dep)
+      ::mdp::launch_k_dependent(stencil3_kernel<N, RY, false, true>, grid, threads, smem, st, *p, sel, x, ldx, y, ldy,
+                                zchunk, jr, omega, G);
+    else
+      ::mdp::launch_k(stencil3_kernel<N, RY, false, true>, grid, threads, smem, st, *p, sel, x, ldx, y, ldy, zchunk, jr,
+                      omega, G);
+  } else if (jr) {
     if (dep)
       ::mdp::launch_k_dependent(stencil3_kernel<N, RY, true>, grid, threads, smem, st, *p, sel, x, ldx, y, ldy, zchunk,
                                 jr, omega, G);
@@ -788,15 +799,17 @@ static void launch_stencil3_t(dim3 grid, int threads, size_t smem, cudaStream_t 
 // resident blocks per SM of one instantiation at this launch shape (registers AND shared memory;
 // the 156-register consumer holds 129^3 to 2 blocks of 192 threads per SM, not the 5 its ring would allow)
 template <int N, int RY>
-static int stencil3_blocks_per_sm(int threads, size_t smem, bool jac, int n) {
-  static int cache[2][2] = {{0, 0}, {0, 0}};  // [jac] -> (n, blocks)
-  int* c = cache[jac ? 1 : 0];
+static int stencil3_blocks_per_sm(int threads, size_t smem, bool jac, int n, bool lc) {
+  static int cache[3][2] = {{0, 0}, {0, 0}, {0, 0}};  // [plain | Jacobi | plain last-column] -> (n, blocks)
+  int* c = cache[jac ? 1 : (lc ? 2 : 0)];
   const int key = n * 2048 + threads;
   if (c[0] == key && c[1] > 0) return c[1];
   launch_stencil3_attr<N, RY>();
   int nb = 0;
-  cudaError_t e = jac ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, stencil3_kernel<N, RY, true>, threads, smem)
-                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, stencil3_kernel<N, RY, false>, threads, smem);
+  cudaError_t e =
+      jac  ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, stencil3_kernel<N, RY, true>, threads, smem)
+      : lc ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, stencil3_kernel<N, RY, false, true>, threads, smem)
+           : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, stencil3_kernel<N, RY, false>, threads, smem);
   if (e != cudaSuccess || nb < 1) {
     cudaGetLastError();
     nb = 1;
@@ -815,7 +828,7 @@ static int launch_stencil3(const mdp_problem* p, int32_t nsel, const int32_t* se
   static const int ry_env = env_int("MDP_STENCIL_RY", 0);
   const int RY = ry_env == 2 || ry_env == 4 || ry_env == 8 ? ry_env : (n <= 48 ? 2 : 4);
   const int S = kSt3;
-  const bool lastcol = jr == nullptr && p->bc3d != 0 && n > 32 && ((n - 1) & 31) == 0;  // see stencil3_consumer
+  const bool lastcol = jr == nullptr && nsel >= 2 && p->bc3d != 0 && n > 32 && ((n - 1) & 31) == 0;  // see stencil3_consumer
   const int tiles_x = lastcol ? (n - 1) / 32 : ceil_div(n, 32);
   const int bands = ceil_div(n, RY);
   const int threads = 32 * (tiles_x + 1);
@@ -827,7 +840,7 @@ static int launch_stencil3(const mdp_problem* p, int32_t nsel, const int32_t* se
   // steps' worth, traced) and then one step per plane of its chunk plus 2 halo planes; blocks run in waves
   // of (resident blocks per SM) x SMs.  Pick the chunk count that minimises waves x chain length.
   int per_sm = 1;
-#define MDP_ST3O(NN, R) per_sm = stencil3_blocks_per_sm<NN, R>(threads, smem, jr != nullptr, n)
+#define MDP_ST3O(NN, R) per_sm = stencil3_blocks_per_sm<NN, R>(threads, smem, jr != nullptr, n, lastcol)
   if (RY == 2) {
     switch (n) {
       case 17: MDP_ST3O(17, 2); break;
@@ -871,7 +884,7 @@ static int launch_stencil3(const mdp_problem* p, int32_t nsel, const int32_t* se
   if (gat) G.nblk = ceil_div(p->qmax, (tiles_x + 1) * 2);  // ~2 quadrature rows per warp
   dim3 grid(G.nblk + bands * zch, nsel);
 #define MDP_ST3L(NN, R) \
-  launch_stencil3_t<NN, R>(grid, threads, smem, st, p, sel, x, ldx, y, ldy, zchunk, jr, omega, G)
+  launch_stencil3_t<NN, R>(grid, threads, smem, st, p, sel, x, ldx, y, ldy, zchunk, jr, omega, G, lastcol)
   if (RY == 2) {
     switch (n) {
       case 17: MDP_ST3L(17, 2); break;
